@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 coupled MLMC level sampler (BASELINE.json metric:
+coupled fine path-steps/s per level, % of the FP64 roofline).
+
+Workload (BASELINE.json configs[4], "C5"): reference profile (kappa_sigma
+1.3, kappa_tau 0.5, u* 0.2, H 1, eps_reg 0.01), z0 = 500 m (x0 = 0.5),
+u0 = 0.1, T = 1000 s (T = 1), M0 = 1, level l = 10 (1024 fine + 512 coarse
+steps), symplectic Euler, fp64, mean-position QoI, Philox seed 42, N coupled
+paths per GPU (default 2^25).  One step = one accumulate_samples call over
+the N paths (level sampler + moment reduction).  Weak scaling: rank r owns
+sample indices [r N, (r+1) N) (contiguous super-blocks), and for N > 1 the
+per-rank moments meet in one NCCL all-gather per step.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--paths N] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+# Algorithmic FP64-pipe ops per coupled fine path-step.
+W_ALG = {0: 181.0, 1: 273.0, 2: 416.0}
+IG_NAME = {0: "se", 1: "gl", 2: "baoab"}
+LEVEL = 10
+SEED = 42
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--paths", type=int, default=1 << 25, help="coupled paths per GPU per step")
+    ap.add_argument("--integrator", default="se", choices=["se", "gl", "baoab"])
+    ap.add_argument("--level", type=int, default=LEVEL)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="target wall time of the CPU baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def problem_c(ig: int):
+    from paper_1612_07717_b200 import ablmc
+    return ablmc.Problem.make(ablmc.ModelParams(), ablmc.Integrator(ig), ablmc.QoISpec(), 0.5, 0.1,
+                              1.0, 1, SEED)
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------ CPU reference
+def reference_sample(ig: int, level: int, target_s: float, threads: int):
+    """Time the reference's own accumulate_samples (oracle/_ref, unmodified
+    headers, std::thread pool) on a bounded sample; returns (path-steps/s,
+    samples, seconds)."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib as O
+    R = O.ref()
+    if R is None:
+        raise RuntimeError("oracle/_ref/libablmc_ref.so is missing (built by __graft_entry__.build)")
+    pr = problem_c(ig)
+    Mf = 1 << level
+    n = max(threads * 64, 4096)
+    secs = C.c_double()
+    while True:
+        st = O.Stats(1)
+        rc = R.ref_accumulate_samples(C.byref(pr._c), level, 0, n, threads, C.byref(st.c),
+                                      C.byref(secs))
+        if rc != 0:
+            raise RuntimeError(R.ref_last_error().decode())
+        if secs.value >= 0.5 * target_s or n > (1 << 30):
+            break
+        n = int(n * min(64.0, max(2.0, target_s / max(secs.value, 1e-3))))
+    return n * Mf / secs.value, n, secs.value
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # rank 0 alone runs the CPU reference arm
+    ig = {"se": 0, "gl": 1, "baoab": 2}[a.integrator]
+    threads = host_threads()
+    step_s = max(1.0, 60.0 / max(1, a.steps + a.warmup))  # whole run within ~1-2 min
+    rate, n, _ = reference_sample(ig, a.level, step_s, threads)
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib as O
+    R = O.ref()
+    pr = problem_c(ig)
+    secs = C.c_double()
+    times = []
+    for i in range(a.warmup + a.steps):
+        st = O.Stats(1)
+        R.ref_accumulate_samples(C.byref(pr._c), a.level, i * n, n, threads, C.byref(st.c),
+                                 C.byref(secs))
+        if i >= a.warmup:
+            times.append(secs.value)
+    Mf = 1 << a.level
+    t = statistics.mean(times)
+    value = n * Mf / t
+    line = {
+        "impl": "reference", "metric": "coupled fine path-steps/s (level sampler)",
+        "value": value, "unit": "path-steps/s", "n_gpus": a.gpus, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (Philox seed 42)",
+        "config": {"workload": f"C5: level {a.level} coupled pair, {IG_NAME[ig]}, reference profile, "
+                               f"x0=0.5, u0=0.1, T=1, M0=1; bounded CPU sample of {n} paths/step",
+                   "level": a.level, "paths_per_step": n},
+        "cpu_baseline": {"value": value, "unit": "path-steps/s", "cores": threads,
+                         "kind": "reference",
+                         "sample": f"{n} coupled paths x {Mf} fine steps per step; reference "
+                                   f"accumulate_samples with {threads} worker threads"},
+        "e2e": {"value": value, "unit": "path-steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, device: int):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- B200 arm
+def run_b200(a):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_1612_07717_b200 import ablmc
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ablmc.init(local)
+    stream = torch.cuda.current_stream()
+    ablmc.set_stream(stream.cuda_stream)
+    lib = ablmc.lib()
+
+    ig = {"se": 0, "gl": 1, "baoab": 2}[a.integrator]
+    level = a.level
+    Mf = 1 << level
+    N = a.paths
+    pr = problem_c(ig)
+    first = rank * N
+    pc = C.byref(pr._c)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
+    res_s = torch.zeros(2, dtype=torch.float64, device="cuda")
+    res_c = torch.zeros(2, dtype=torch.int64, device="cuda")
+    gat_s = torch.zeros(world, 2, dtype=torch.float64, device="cuda")
+    gat_c = torch.zeros(world, 2, dtype=torch.int64, device="cuda")
+
+    def device_step():
+        rc = lib.ablmc_accumulate_device(pc, level, first, N)
+        if rc:
+            ablmc._check(rc)
+        launches = lib.ablmc_last_launch_count()
+        if world > 1:  # one collective per step: all-gather of the per-rank moments
+            lib.ablmc_copy_device_result(C.c_void_p(res_s.data_ptr()), C.c_void_p(res_c.data_ptr()))
+            dist.all_gather_into_tensor(gat_s, res_s)
+            dist.all_gather_into_tensor(gat_c, res_c)
+        return launches
+
+    # ---- value: device-resident, CUDA events on the launching stream
+    for _ in range(a.warmup):
+        device_step()
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(a.steps)]
+    launches = 0
+    with ClockSampler(local) as clk:
+        for i in range(a.steps):
+            flush.zero_()  # L2 flush between timed iterations (outside the events)
+            barrier()
+            ev[i][0].record(stream)
+            launches += device_step()
+            ev[i][1].record(stream)
+        barrier()
+    ms = [s.elapsed_time(e) for s, e in ev]
+    total_ms = max_over_ranks(sum(ms))
+    ms_per_step = total_ms / a.steps
+    value = world * N * Mf / (ms_per_step * 1e-3)
+
+    # moments of the last step (sanity: E[Y_10], all ranks)
+    acc = ablmc.LevelStats().init(level, pr.h_level(level), 1)
+    v = acc._view()
+    ablmc._check(lib.ablmc_fetch_device_result(pc, level, C.byref(v)))
+    acc._take(v)
+
+    # ---- dominant kernel share: level kernel alone, one launch, events
+    # (N paths in one chunk of 2^25 -> one K1 launch dominates the step)
+    fp64_rate = C.c_double()
+    ablmc._check(lib.ablmc_probe_fp64_rate(C.byref(fp64_rate)))
+    achieved = value / world * W_ALG[ig]  # per-GPU algorithmic FP64 lane-ops/s
+    peak = fp64_rate.value
+
+    # ---- e2e: public API, host LevelStats in/out, sharded + gathered
+    e2e_times = []
+    n_sb = ablmc.num_superblocks(N)
+    for i in range(a.warmup + a.steps):
+        barrier()
+        t0 = time.perf_counter()
+        sums, cnts = ablmc.accumulate_partials(pr, level, first, N, 0, n_sb)
+        if world > 1:
+            t_s = torch.from_numpy(sums).cuda()
+            t_c = torch.from_numpy(cnts).cuda()
+            g_s = [torch.empty_like(t_s) for _ in range(world)]
+            g_c = [torch.empty_like(t_c) for _ in range(world)]
+            dist.all_gather(g_s, t_s)
+            dist.all_gather(g_c, t_c)
+            sums = torch.cat(g_s).cpu().numpy()
+            cnts = torch.cat(g_c).cpu().numpy()
+        e2e_acc = ablmc.LevelStats().init(level, pr.h_level(level), 1)
+        ablmc.merge_partials(e2e_acc, pr, level, sums, cnts)
+        t1 = time.perf_counter()
+        if i >= a.warmup:
+            e2e_times.append(t1 - t0)
+    e2e_t = max_over_ranks(statistics.mean(e2e_times))
+    e2e_value = world * N * Mf / e2e_t
+    h2d = C.sizeof(pr._c)  # the problem descriptor (kernel parameters) per call
+    d2h = n_sb * (2 * 1 + 2) * 8  # super-block partials
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    line = {
+        "metric": "coupled fine path-steps/s (level sampler)", "value": value,
+        "unit": "path-steps/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (Philox seed 42)",
+        "config": {"workload": f"C5: level {level} coupled pair ({Mf} fine + {Mf // 2} coarse steps), "
+                               f"{IG_NAME[ig]}, reference profile, x0=0.5, u0=0.1, T=1, M0=1, "
+                               f"mean-position QoI",
+                   "paths_per_gpu": N, "level": level, "integrator": IG_NAME[ig],
+                   "l2": "flushed between timed steps (256 MB write); kernel state is register-resident",
+                   "parallelism": f"dp{world} (sample shards, 1 NCCL all-gather/step)"},
+        "e2e": {"value": e2e_value, "unit": "path-steps/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12,
+                     "unit": "FP64 Tops/s (pipe lane-ops)", "frac": achieved / peak,
+                     "traffic": None,
+                     "note": f"achieved = path-steps/s/GPU x W_alg={W_ALG[ig]:.0f} FP64-pipe ops per "
+                             "coupled fine path-step (SURVEY.md 8(d)); peak = DFMA probe measured "
+                             "in this run (MEASURED_PEAKS.json has no FP64 entry)"},
+        "clocks": clk.summary(),
+        "estimate": {"mean_y": acc.mean(), "n": acc.n, "failed": acc.failed},
+    }
+    if not a.no_cpu_baseline and world == 1:
+        threads = host_threads()
+        rate, n_cpu, secs = reference_sample(ig, level, a.cpu_seconds, threads)
+        line["cpu_baseline"] = {"value": rate, "unit": "path-steps/s", "cores": threads,
+                                "kind": "reference",
+                                "sample": f"{n_cpu} coupled paths x {Mf} fine steps in {secs:.1f} s, "
+                                          f"reference accumulate_samples, {threads} threads"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_b200(a)
+
+
+if __name__ == "__main__":
+    main()

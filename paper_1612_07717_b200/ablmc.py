@@ -1,0 +1,461 @@
+"""Python mirror of the reference's ablmc API for the device level sampler.
+
+Names, argument meaning and error behaviour follow the reference headers
+(/root/reference/proj/include/ablmc): ``ModelParams`` (model.hpp:28-48),
+``QoISpec`` (qoi.hpp:107-142), ``Problem`` (estimators.hpp:26-94),
+``LevelStats`` (stats.hpp:26-88), ``accumulate_samples`` (stats.hpp:96-136),
+``check_failure_budget`` (stats.hpp:139-143), ``run_mlmc`` / ``run_stmc`` /
+``decay_sweep`` (estimators.hpp:230-431).  Every sampling call goes through
+the C ABI of ``libablmc_b200.so`` (sm_100a kernels); nothing here computes a
+sample on the CPU.
+
+Exceptions: std::invalid_argument -> ``ValueError``; std::runtime_error ->
+``RuntimeError``; SampleFailureError -> ``SampleFailureError``; CUDA / no
+device -> ``CudaError``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import capi
+
+_P = C.pointer
+
+
+class SampleFailureError(RuntimeError):
+    """More than 0.01% of a level's samples failed (stats.hpp:19-22)."""
+
+
+class CudaError(RuntimeError):
+    """CUDA failure or no usable sm_100a device."""
+
+
+class Integrator(enum.IntEnum):
+    se = capi.SE
+    gl = capi.GL
+    baoab = capi.BAOAB
+
+
+class QoIKind(enum.IntEnum):
+    mean_position = capi.QOI_MEAN_POSITION
+    smoothed_indicator = capi.QOI_SMOOTHED_INDICATOR
+    raw_indicator = capi.QOI_RAW_INDICATOR
+    binned_field = capi.QOI_BINNED_FIELD
+
+
+class Profile(enum.IntEnum):
+    reference = capi.PROFILE_REFERENCE
+    constant = capi.PROFILE_CONSTANT  # extension (BASELINE config 1), parity unpinned
+    floored = capi.PROFILE_FLOORED    # extension (BASELINE configs 2-5 as written), parity unpinned
+
+
+def lib() -> C.CDLL:
+    return capi.load()
+
+
+def _check(rc: int) -> None:
+    if rc == capi.ABLMC_OK:
+        return
+    msg = lib().ablmc_last_error().decode()
+    if rc == capi.ABLMC_ERR_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if rc == capi.ABLMC_ERR_RUNTIME:
+        raise RuntimeError(msg)
+    if rc == capi.ABLMC_ERR_SAMPLE_FAILURE:
+        raise SampleFailureError(msg)
+    raise CudaError(msg)
+
+
+def init(device: int = -1) -> None:
+    _check(lib().ablmc_init(device))
+
+
+def set_stream(cuda_stream: int | None) -> None:
+    """Launch on this cudaStream_t (e.g. ``torch.cuda.current_stream().cuda_stream``)."""
+    lib().ablmc_set_stream(C.c_void_p(cuda_stream) if cuda_stream else None)
+
+
+@dataclass
+class ModelParams:  # model.hpp:28-35
+    kappa_sigma: float = 1.3
+    kappa_tau: float = 0.5
+    u_star: float = 0.2
+    H: float = 1.0
+    eps_reg: float = 0.01
+    x_ref: float = 1.0
+    noise_scale: float = 1.0
+
+    def validate(self) -> None:  # model.hpp:37-47
+        p = Problem.make(self, Integrator.gl, QoISpec(), 0.5, 0.0, 1.0, 1, 0, validate=False)
+        _check(lib().ablmc_problem_validate(_P(p._c)))
+
+    def c(self) -> capi.ModelParamsC:
+        return capi.ModelParamsC(self.kappa_sigma, self.kappa_tau, self.u_star, self.H,
+                                 self.eps_reg, self.x_ref, self.noise_scale)
+
+
+def equidistant_edges(bins: int, H: float) -> list[float]:  # qoi.hpp:144-151
+    if bins < 1:
+        raise ValueError("equidistant_edges: bins must be >= 1")
+    e = [H * float(i) / float(bins) for i in range(bins + 1)]
+    e[0], e[-1] = 0.0, H
+    return e
+
+
+@dataclass
+class QoISpec:  # qoi.hpp:107-113
+    kind: QoIKind = QoIKind.mean_position
+    a: float = 0.1055
+    b: float = 0.1555
+    r: int = 4
+    delta: float = 0.1
+    bin_edges: Sequence[float] = field(default_factory=list)
+
+    def size(self) -> int:
+        return len(self.bin_edges) - 1 if self.kind == QoIKind.binned_field else 1
+
+
+@dataclass
+class SampleOptions:  # coupling.hpp:216-221
+    signs_on: bool = True
+    adaptive: bool = False
+    x_adapt: float = 0.05
+
+
+class Problem:
+    """Problem (estimators.hpp:26-94) as a C descriptor; build with make()."""
+
+    def __init__(self) -> None:
+        self._c = capi.ProblemC()
+        lib().ablmc_problem_defaults(_P(self._c))
+        self._edges = None
+        self.qoi = QoISpec()
+
+    @staticmethod
+    def make(params: ModelParams, ig: Integrator, qoi: QoISpec, x0: float, u0: float, T: float,
+             m0: int, seed: int, opt: SampleOptions | None = None, *,
+             profile: Profile = Profile.reference, random_u0: bool = False,
+             const_sigma_u: float = 1.3, const_tau: float = 0.1, sigma_floor: float = 1e-3,
+             tau_min: float = 1e-5, tau_max: float = 1.0, validate: bool = True) -> "Problem":
+        opt = opt or SampleOptions()
+        pr = Problem()
+        c = pr._c
+        c.params = params.c()
+        c.integrator = int(ig)
+        c.signs_on = 1 if opt.signs_on else 0
+        c.adaptive = 1 if opt.adaptive else 0
+        c.x_adapt = opt.x_adapt
+        c.qoi.kind = int(qoi.kind)
+        c.qoi.a, c.qoi.b, c.qoi.r, c.qoi.delta = qoi.a, qoi.b, int(qoi.r), qoi.delta
+        if qoi.kind == QoIKind.binned_field:
+            pr._edges = (C.c_double * len(qoi.bin_edges))(*qoi.bin_edges)
+            c.qoi.n_edges = len(qoi.bin_edges)
+            c.qoi.bin_edges = C.cast(pr._edges, C.POINTER(C.c_double))
+        c.x0, c.u0, c.T, c.m0, c.seed = x0, u0, T, int(m0), int(seed) & ((1 << 64) - 1)
+        c.profile = int(profile)
+        c.random_u0 = 1 if random_u0 else 0
+        c.const_sigma_u, c.const_tau = const_sigma_u, const_tau
+        c.sigma_floor, c.tau_min, c.tau_max = sigma_floor, tau_min, tau_max
+        pr.qoi = qoi
+        if validate:
+            _check(lib().ablmc_problem_validate(_P(c)))
+        return pr
+
+    # accessors mirroring the reference's public fields
+    @property
+    def integrator(self) -> Integrator:
+        return Integrator(self._c.integrator)
+
+    @property
+    def m0(self) -> int:
+        return self._c.m0
+
+    @property
+    def T(self) -> float:
+        return self._c.T
+
+    @property
+    def seed(self) -> int:
+        return self._c.seed
+
+    def with_seed(self, seed: int) -> "Problem":
+        q = Problem()
+        C.memmove(C.addressof(q._c), C.addressof(self._c), C.sizeof(capi.ProblemC))
+        q._edges, q.qoi = self._edges, self.qoi
+        q._c.seed = int(seed)
+        return q
+
+    def dim(self) -> int:
+        return int(lib().ablmc_qoi_dim(_P(self._c)))
+
+    def h_level(self, level: int) -> float:  # estimators.hpp:39
+        return self._c.T / float(self._c.m0 << level)
+
+    def check_se_stability(self, h: float) -> None:  # estimators.hpp:86-93
+        _check(lib().ablmc_check_se_stability(_P(self._c), h))
+
+
+class LevelStats:
+    """LevelStats (stats.hpp:26-88) with numpy sums."""
+
+    def __init__(self) -> None:
+        self.init(0, 0.0, 1)
+
+    def init(self, level: int, h: float, dim: int) -> "LevelStats":
+        self.level, self.h, self.dim = int(level), float(h), int(dim)
+        self.sum_y = np.zeros(self.dim)
+        self.sum_y2 = np.zeros(self.dim)
+        self.n = self.failed = self.cost_steps = 0
+        return self
+
+    def attempts(self) -> int:
+        return self.n + self.failed
+
+    def add(self, y: Sequence[float], steps: int) -> None:  # stats.hpp:46-53
+        for i in range(self.dim):
+            self.sum_y[i] += y[i]
+            self.sum_y2[i] += y[i] * y[i]
+        self.n += 1
+        self.cost_steps += steps
+
+    def merge(self, o: "LevelStats") -> None:  # stats.hpp:55-63
+        self.sum_y += o.sum_y
+        self.sum_y2 += o.sum_y2
+        self.n += o.n
+        self.failed += o.failed
+        self.cost_steps += o.cost_steps
+
+    def mean(self, i: int = 0) -> float:
+        return float(self.sum_y[i]) / float(self.n)
+
+    def variance(self, i: int = 0) -> float:  # stats.hpp:67-71
+        if self.n < 2:
+            return 0.0
+        m = float(self.sum_y[i]) / float(self.n)
+        return max(0.0, (float(self.sum_y2[i]) - float(self.n) * m * m) / float(self.n - 1))
+
+    def max_variance(self) -> float:
+        return max([0.0] + [self.variance(i) for i in range(self.dim)])
+
+    def max_abs_mean(self) -> float:
+        return max([0.0] + [abs(self.mean(i)) for i in range(self.dim)])
+
+    def std_error(self, i: int = 0) -> float:
+        return (self.variance(i) / float(self.n)) ** 0.5 if self.n > 0 else 0.0
+
+    # C view sharing the numpy buffers (add-merge happens in place)
+    def _view(self) -> capi.LevelStatsC:
+        v = capi.LevelStatsC()
+        v.level, v.h, v.dim = self.level, self.h, self.dim
+        v.sum_y = self.sum_y.ctypes.data_as(C.POINTER(C.c_double))
+        v.sum_y2 = self.sum_y2.ctypes.data_as(C.POINTER(C.c_double))
+        v.n, v.failed, v.cost_steps = self.n, self.failed, self.cost_steps
+        return v
+
+    def _take(self, v: capi.LevelStatsC) -> None:
+        self.n, self.failed, self.cost_steps = v.n, v.failed, v.cost_steps
+
+
+def accumulate_samples(acc: LevelStats, first: int, count: int, pr: Problem, level: int) -> None:
+    """Device replacement for ``accumulate_samples(acc, first, count, workers,
+    pr.level_sampler(level))`` (stats.hpp:96-136, estimators.hpp:60-72)."""
+    if acc.dim != pr.dim():
+        raise ValueError("LevelStats dim does not match the QoI size")
+    v = acc._view()
+    _check(lib().ablmc_accumulate_samples(_P(pr._c), int(level), int(first), int(count), _P(v)))
+    acc._take(v)
+
+
+def accumulate_paths(acc: LevelStats, first: int, count: int, pr: Problem, M: int,
+                     stream_level: int = 0) -> None:
+    """Device replacement for ``accumulate_samples(..., pr.path_sampler(M, stream_level))``."""
+    v = acc._view()
+    _check(lib().ablmc_accumulate_paths(_P(pr._c), int(M), int(stream_level), int(first),
+                                        int(count), _P(v)))
+    acc._take(v)
+
+
+def check_failure_budget(acc: LevelStats) -> None:  # stats.hpp:139-143
+    v = acc._view()
+    _check(lib().ablmc_check_failure_budget(_P(v)))
+
+
+# --------------------------------------------------------------- sharding
+def num_superblocks(count: int) -> int:
+    return int(lib().ablmc_num_superblocks(int(count)))
+
+
+def accumulate_partials(pr: Problem, level: int, first: int, count: int, sb_begin: int,
+                        sb_end: int, M: int = 0, stream_level: int = 0):
+    """Super-block partials [sb_begin, sb_end) -> (sums[n,2*dim], counts[n,2])."""
+    n = sb_end - sb_begin
+    dim = pr.dim()
+    sums = np.zeros((max(n, 0), 2 * dim))
+    counts = np.zeros((max(n, 0), 2), dtype=np.int64)
+    _check(lib().ablmc_accumulate_partials(
+        _P(pr._c), int(level), int(M), int(stream_level), int(first), int(count), int(sb_begin),
+        int(sb_end), sums.ctypes.data_as(C.POINTER(C.c_double)),
+        counts.ctypes.data_as(C.POINTER(C.c_int64))))
+    return sums, counts
+
+
+def merge_partials(acc: LevelStats, pr: Problem, level: int, sums: np.ndarray, counts: np.ndarray,
+                   M: int = 0) -> None:
+    sums = np.ascontiguousarray(sums, dtype=np.float64)
+    counts = np.ascontiguousarray(counts, dtype=np.int64)
+    v = acc._view()
+    _check(lib().ablmc_merge_partials(_P(pr._c), int(level), int(M), int(sums.shape[0]),
+                                      sums.ctypes.data_as(C.POINTER(C.c_double)),
+                                      counts.ctypes.data_as(C.POINTER(C.c_int64)), _P(v)))
+    acc._take(v)
+
+
+# ------------------------------------------------------------- oracle mode
+PAIR_DTYPE = np.dtype([("fx", "f8"), ("fu", "f8"), ("fpar", "i4"), ("fok", "i4"), ("fn", "i8"),
+                       ("cx", "f8"), ("cu", "f8"), ("cpar", "i4"), ("cok", "i4"), ("cn", "i8")])
+PATH_DTYPE = np.dtype([("x", "f8"), ("u", "f8"), ("parity", "i4"), ("ok", "i4"), ("n_refl", "i8")])
+
+
+def simulate_pairs(pr: Problem, level: int, first: int, count: int,
+                   xi: Optional[np.ndarray] = None) -> np.ndarray:
+    """simulate_pair (coupling.hpp:64-105) for samples [first, first+count).
+    xi[count, M_f]: host-supplied normals (oracle mode), else Philox."""
+    out = np.zeros(count, dtype=PAIR_DTYPE)
+    xp = None
+    if xi is not None:
+        xi = np.ascontiguousarray(xi, dtype=np.float64)
+        if xi.shape != (count, pr.m0 << level):
+            raise ValueError("xi must have shape (count, m0 << level)")
+        xp = xi.ctypes.data_as(C.POINTER(C.c_double))
+    _check(lib().ablmc_pair_states(_P(pr._c), int(level), int(first), int(count), xp,
+                                   out.ctypes.data_as(C.POINTER(capi.PairStateC))))
+    return out
+
+
+def simulate_paths(pr: Problem, M: int, first: int, count: int, stream_level: int = 0,
+                   xi: Optional[np.ndarray] = None) -> np.ndarray:
+    out = np.zeros(count, dtype=PATH_DTYPE)
+    xp = None
+    if xi is not None:
+        xi = np.ascontiguousarray(xi, dtype=np.float64)
+        if xi.shape != (count, M):
+            raise ValueError("xi must have shape (count, M)")
+        xp = xi.ctypes.data_as(C.POINTER(C.c_double))
+    _check(lib().ablmc_path_states(_P(pr._c), int(M), int(stream_level), int(first), int(count),
+                                   xp, out.ctypes.data_as(C.POINTER(capi.PathStateC))))
+    return out
+
+
+def normals(seed: int, level: int, idx: int, k0: int, n: int) -> np.ndarray:
+    """NoiseStream(seed, level, idx).normal_at(k0 + j) on the device (noise.hpp:57-75)."""
+    out = np.zeros(n)
+    _check(lib().ablmc_normals(int(seed), int(level), int(idx), int(k0), int(n),
+                               out.ctypes.data_as(C.POINTER(C.c_double))))
+    return out
+
+
+# ----------------------------------------------------------------- drivers
+@dataclass
+class MlmcOptions:  # estimators.hpp:271-278
+    pilot_n: int = 10000
+    pilot_levels_max: int = 4
+    init_n: int = 1000
+    l_max: int = 16
+    bias_fit: Optional[tuple[float, float]] = None  # (alpha, c1)
+
+
+@dataclass
+class RunResult:  # estimators.hpp:197-210
+    estimate: list
+    stat_error: list
+    bias_estimate: float
+    alpha: float
+    c1: float
+    levels_used: int
+    level_stats: list
+    total_cost_steps: int
+    pilot_cost_steps: int
+    failed_samples: int
+    wall_seconds: float
+    n_warnings: int
+
+
+def _result(r: capi.RunResultC, pr: Problem, est: np.ndarray, err: np.ndarray) -> RunResult:
+    levels = []
+    for l in range(r.n_levels):
+        st = LevelStats().init(l, r.level_h[l], 1)
+        st.sum_y[0], st.sum_y2[0] = r.level_sum_y[l], r.level_sum_y2[l]
+        st.n, st.failed, st.cost_steps = r.level_n[l], r.level_failed[l], r.level_cost[l]
+        levels.append(st)
+    return RunResult(list(est), list(err), r.bias_estimate, r.alpha, r.c1, r.levels_used, levels,
+                     r.total_cost_steps, r.pilot_cost_steps, r.failed_samples, r.wall_seconds,
+                     r.n_warnings)
+
+
+def run_mlmc(pr: Problem, eps: float, o: MlmcOptions | None = None) -> RunResult:
+    o = o or MlmcOptions()
+    oc = capi.MlmcOptionsC()
+    lib().ablmc_mlmc_options_defaults(_P(oc))
+    oc.pilot_n, oc.pilot_levels_max, oc.init_n, oc.l_max = o.pilot_n, o.pilot_levels_max, o.init_n, o.l_max
+    if o.bias_fit is not None:
+        oc.use_bias_fit, (oc.alpha, oc.c1) = 1, o.bias_fit
+    r = capi.RunResultC()
+    est, err = np.zeros(pr.dim()), np.zeros(pr.dim())
+    r.est_vec = est.ctypes.data_as(C.POINTER(C.c_double))
+    r.err_vec = err.ctypes.data_as(C.POINTER(C.c_double))
+    _check(lib().ablmc_run_mlmc(_P(pr._c), float(eps), _P(oc), _P(r)))
+    return _result(r, pr, est, err)
+
+
+def run_stmc(pr: Problem, M_L: int, eps: float, fixed_n: int = 0) -> RunResult:
+    r = capi.RunResultC()
+    est, err = np.zeros(pr.dim()), np.zeros(pr.dim())
+    r.est_vec = est.ctypes.data_as(C.POINTER(C.c_double))
+    r.err_vec = err.ctypes.data_as(C.POINTER(C.c_double))
+    _check(lib().ablmc_run_stmc(_P(pr._c), int(M_L), float(eps), int(fixed_n), _P(r)))
+    return _result(r, pr, est, err)
+
+
+@dataclass
+class DecayRow:  # estimators.hpp:403-411
+    level: int
+    h: float
+    var_y: float
+    mean_y: float
+    se_mean: float
+    n: int
+    cost_steps: int
+
+
+def decay_sweep(pr: Problem, l_min: int, l_max: int, n_per_level: int) -> list[DecayRow]:
+    rows = (capi.DecayRowC * (l_max - l_min + 1))()
+    _check(lib().ablmc_decay_sweep(_P(pr._c), int(l_min), int(l_max), int(n_per_level), rows))
+    return [DecayRow(r.level, r.h, r.var_y, r.mean_y, r.se_mean, r.n, r.cost_steps) for r in rows]
+
+
+def fit_power_law(h: Sequence[float], v: Sequence[float]) -> tuple[float, float]:
+    """estimators.hpp:107-123 -> (exponent, log_prefactor). Host arithmetic only."""
+    import math
+    if len(h) != len(v) or len(h) < 2:
+        raise ValueError("fit_power_law: need at least two points")
+    sx = sy = sxx = sxy = 0.0
+    n = float(len(h))
+    for hi, vi in zip(h, v):
+        if not vi > 0.0:
+            raise ValueError("fit_power_law: values must be positive")
+        x, y = math.log(hi), math.log(vi)
+        sx += x
+        sy += y
+        sxx += x * x
+        sxy += x * y
+    slope = (n * sxy - sx * sy) / (n * sxx - sx * sx)
+    return slope, (sy - slope * sx) / n
+
+
+def variance_decay_slope(rows: Sequence[DecayRow]) -> float:  # estimators.hpp:434-441
+    return fit_power_law([r.h for r in rows], [r.var_y for r in rows])[0]

@@ -1,0 +1,57 @@
+// kernels.h — internal launch interface between the C-ABI host code
+// (capi.cpp) and the sm_100a kernels (level_kernels.cu).  Not public.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "ablmc_device.cuh"
+
+#define ABLMC_TILE 256                 // samples per CTA tile
+#define ABLMC_TILES_PER_BLOCK 16       // 16 * 256 = 4096 = reference block_size (stats.hpp:100)
+#define ABLMC_BLOCKS_PER_SUPER 1024    // 1024 * 4096 = 2^22 = ABLMC_SUPERBLOCK
+#define ABLMC_MAX_POLY 14
+
+// Everything one launch needs, passed by value (kernel-parameter constant bank).
+struct KernelArgs {
+  ablmc_dev::DevModel model;
+  double x0, u0;
+  double h, sqrt_h;         // fine step T/M and sqrt(h)
+  double h2, sqrt_h2;       // coarse step 2h and sqrt(2h)
+  double h_half, h2_half;   // 0.5*h, 0.5*(2h) (BAOAB half steps)
+  int64_t M;                // fine steps (path: steps)
+  int64_t first;            // reference `first` (sample index of offset 0)
+  int64_t offset;           // offset of this launch's sample 0 from `first`
+  int64_t n;                // samples in this launch
+  uint32_t k0, k1;          // Philox key of stream (seed, level)
+  int signs_on;
+  int random_u0;
+  int qoi_kind;
+  int dim;
+  double qa, qb, delta;
+  int poly_n;               // r + 2 coefficients
+  double poly[ABLMC_MAX_POLY];
+  const double* edges;      // device copy of bin edges (binned field)
+};
+
+struct StateOut {
+  double fx, fu, cx, cu;
+  int fpar, cpar;
+  int fn, cn;
+  int ok, pad;
+};
+
+cudaError_t launch_level(const KernelArgs& a, int ig, bool coupled, double* tile_sums,
+                         int* tile_cnt, cudaStream_t st);
+cudaError_t launch_states(const KernelArgs& a, int ig, bool coupled, const double* xi,
+                          StateOut* out, cudaStream_t st);
+cudaError_t launch_merge_tiles(int64_t n_tiles, int dim, const double* ts, const int* tc,
+                               double* bs, long long* bc, cudaStream_t st);
+cudaError_t launch_merge_blocks(int64_t n_blk, int dim, const double* bs, const long long* bc,
+                                double* ss, long long* sc, int64_t sb_base, cudaStream_t st);
+cudaError_t launch_merge_super(int64_t n_sb, int dim, const double* ss, const long long* sc,
+                               double* rs, long long* rc, cudaStream_t st);
+cudaError_t launch_normals(uint32_t k0, uint32_t k1, uint64_t idx, uint64_t kstart, int64_t n,
+                           double* out, cudaStream_t st);
+// DFMA throughput probe (FP64 lane-ops/s), see ablmc_probe_fp64_rate.
+cudaError_t probe_fp64(cudaStream_t st, double* lane_ops_per_s);

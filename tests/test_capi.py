@@ -1,0 +1,170 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol the
+public header declares, its struct layouts match the ctypes mirror, and the
+host-side logic (validation, stability rule, failure budget, defaults)
+behaves like the reference (model.hpp:37-47, qoi.hpp:119-141,
+estimators.hpp:86-93, stats.hpp:139-143)."""
+import ctypes as C
+import re
+import subprocess
+import textwrap
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_1612_07717_b200 import ablmc, capi
+
+ROOT = Path(__file__).resolve().parents[1]
+HEADER = ROOT / "include" / "ablmc_b200.h"
+
+
+def declared_functions():
+    text = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+    return sorted(set(re.findall(r"\b(ablmc_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = capi.load()
+    names = declared_functions()
+    assert len(names) >= 25
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(capi.SIGNATURES), "ctypes mirror out of sync with the header"
+    nm = subprocess.run(["nm", "-D", "--defined-only", str(capi.LIB_PATH)], capture_output=True,
+                        text=True, check=True).stdout
+    exported = set(re.findall(r" T (ablmc_\w+)", nm))
+    assert set(names) <= exported
+
+
+def test_abi_version():
+    assert capi.load().ablmc_abi_version() == 1
+
+
+def test_struct_layouts_match_header(tmp_path):
+    structs = {"ablmc_problem": capi.ProblemC, "ablmc_level_stats": capi.LevelStatsC,
+               "ablmc_pair_state": capi.PairStateC, "ablmc_run_result": capi.RunResultC,
+               "ablmc_mlmc_options": capi.MlmcOptionsC, "ablmc_decay_row": capi.DecayRowC,
+               "ablmc_qoi_spec": capi.QoISpecC}
+    lines = [f'printf("{k} %zu\\n", sizeof({k}));' for k in structs]
+    offs = {"ablmc_problem": ["qoi", "x0", "seed", "profile", "random_u0", "tau_max"],
+            "ablmc_run_result": ["level_n", "level_sum_y2", "est_vec", "err_vec"]}
+    for s, fields in offs.items():
+        for f in fields:
+            lines.append(f'printf("{s}.{f} %zu\\n", offsetof({s}, {f}));')
+    src = tmp_path / "l.c"
+    src.write_text(textwrap.dedent(f"""
+        #include <stdio.h>
+        #include <stddef.h>
+        #include "{HEADER}"
+        int main(void) {{ {' '.join(lines)} return 0; }}"""))
+    exe = tmp_path / "l"
+    subprocess.run(["gcc", "-o", str(exe), str(src)], check=True)
+    out = dict(l.split() for l in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                  check=True).stdout.splitlines())
+    for k, cls in structs.items():
+        assert int(out[k]) == C.sizeof(cls), k
+    for s, fields in offs.items():
+        cls = structs[s]
+        for f in fields:
+            assert int(out[f"{s}.{f}"]) == getattr(cls, f).offset, (s, f)
+
+
+def test_problem_defaults_mirror_reference():
+    pr = ablmc.Problem()
+    c = pr._c
+    assert (c.params.kappa_sigma, c.params.kappa_tau, c.params.u_star, c.params.H,
+            c.params.eps_reg, c.params.x_ref, c.params.noise_scale) == (1.3, 0.5, 0.2, 1.0, 0.01,
+                                                                         1.0, 1.0)
+    assert (c.x0, c.u0, c.T, c.m0, c.seed, c.integrator) == (0.05, 0.1, 1.0, 40, 12345, capi.GL)
+    assert (c.qoi.a, c.qoi.b, c.qoi.r, c.qoi.delta) == (0.1055, 0.1555, 4, 0.1)
+    assert c.signs_on == 1 and c.adaptive == 0
+
+
+def mk(**kw):
+    mp = ablmc.ModelParams(**{k: kw.pop(k) for k in list(kw) if hasattr(ablmc.ModelParams, k)})
+    qoi = kw.pop("qoi", ablmc.QoISpec())
+    ig = kw.pop("ig", ablmc.Integrator.gl)
+    return ablmc.Problem.make(mp, ig, qoi, kw.pop("x0", 0.05), 0.1, 1.0, kw.pop("m0", 40), 1,
+                              **kw)
+
+
+def test_validation_errors_mirror_reference():
+    with pytest.raises(ValueError, match="eps_reg"):
+        mk(eps_reg=0.6)  # test_model.cpp:51-54
+    with pytest.raises(ValueError, match="positive"):
+        mk(u_star=0.0)
+    with pytest.raises(ValueError, match="x_ref"):
+        mk(x_ref=2.0)
+    with pytest.raises(ValueError, match="a < b"):
+        mk(qoi=ablmc.QoISpec(kind=ablmc.QoIKind.raw_indicator, a=0.3, b=0.2))
+    with pytest.raises(ValueError, match="span"):
+        mk(qoi=ablmc.QoISpec(kind=ablmc.QoIKind.binned_field, bin_edges=[0.1, 1.0]))
+    with pytest.raises(ValueError, match="increasing"):
+        mk(qoi=ablmc.QoISpec(kind=ablmc.QoIKind.binned_field, bin_edges=[0.0, 0.5, 0.5, 1.0]))
+    with pytest.raises(ValueError, match="r must be"):
+        mk(qoi=ablmc.QoISpec(r=13))
+    with pytest.raises(ValueError, match="adaptive"):
+        mk(opt=ablmc.SampleOptions(adaptive=True))
+    mk()  # defaults validate
+
+
+def test_se_stability_rule():
+    # estimators.hpp:86-93; test_estimators.cpp:158-162 (h = 0.05 >= 0.0387 is rejected)
+    pr = mk(ig=ablmc.Integrator.se, m0=20)
+    with pytest.raises(RuntimeError, match="symplectic Euler unstable"):
+        pr.check_se_stability(0.05)
+    pr.check_se_stability(0.025)
+    mk(ig=ablmc.Integrator.gl).check_se_stability(1.0)  # only SE is checked
+
+
+def test_failure_budget():
+    st = ablmc.LevelStats().init(2, 0.1, 1)
+    st.n, st.failed = 10000, 1
+    ablmc.check_failure_budget(st)  # 1 <= 1e-4 * 10001
+    st.failed = 2
+    with pytest.raises(ablmc.SampleFailureError, match="level 2"):
+        ablmc.check_failure_budget(st)
+
+
+def test_h_level_and_dim():
+    pr = mk(m0=40)
+    assert pr.h_level(3) == 1.0 / 320
+    q = ablmc.QoISpec(kind=ablmc.QoIKind.binned_field, bin_edges=ablmc.equidistant_edges(64, 1.0))
+    assert mk(qoi=q).dim() == 64
+
+
+def test_level_stats_algebra():
+    st = ablmc.LevelStats().init(0, 1.0, 1)  # test_estimators.cpp:305-315
+    for v in (2.0, 4.0, 6.0):
+        st.add([v], 1)
+    assert st.mean() == 4.0 and st.variance() == 4.0
+    assert abs(st.std_error() - (4.0 / 3.0) ** 0.5) <= 1e-14 * (4.0 / 3.0) ** 0.5
+
+
+def test_no_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    acc = ablmc.LevelStats().init(1, 0.0125, 1)
+    with pytest.raises(ablmc.CudaError):
+        ablmc.accumulate_samples(acc, 0, 100, mk(), 1)
+    assert acc.n == 0
+
+
+def test_count_zero_is_a_noop_without_touching_the_device():
+    acc = ablmc.LevelStats().init(1, 0.0125, 1)
+    ablmc.accumulate_samples(acc, 0, 0, mk(), 1)  # stats.hpp:99
+    ablmc.accumulate_samples(acc, 0, -5, mk(), 1)
+    assert acc.n == 0 and acc.sum_y[0] == 0.0
+
+
+def test_merge_partials_is_ordered_add_merge():
+    pr = mk()
+    sums = np.array([[1.0, 1.0], [2.0, 4.0], [0.5, 0.25]])
+    counts = np.array([[3, 0], [4, 1], [2, 0]], dtype=np.int64)
+    acc = ablmc.LevelStats().init(1, 0.0125, 1)
+    acc.sum_y[0] = 10.0
+    ablmc.merge_partials(acc, pr, 1, sums, counts)
+    assert acc.sum_y[0] == ((10.0 + 1.0) + 2.0) + 0.5
+    assert acc.sum_y2[0] == 1.0 + 4.0 + 0.25
+    assert (acc.n, acc.failed, acc.cost_steps) == (9, 1, 9 * (80 + 40))

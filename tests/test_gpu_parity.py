@@ -1,0 +1,332 @@
+"""GPU parity: the sm_100a level sampler (through the C ABI) against the
+reference's outputs (tests/golden/ref_vectors.json, bit-exact reference
+fixtures) and the pinned C oracle.
+
+Tolerances (north star: oracle mode within 1e-12 relative in fp64):
+* host-supplied normals (oracle mode): SE bit-identical; GL/BAOAB within
+  rel 1e-12 or abs 1e-13 (libdevice exp/expm1 vs glibc, <= 1-2 ulp);
+  parity, reflection counts and ok flags exact.
+* in-register Philox normals: the Philox words are integer-exact; Box-Muller
+  log/sin/cos differ from glibc by ulps, so states within rel 1e-10 / abs 1e-12.
+* per-level sums: rel 1e-11 (same samples, different but fixed summation
+  tree); n, failed, cost_steps exact.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle_lib as O
+from conftest import fx
+from paper_1612_07717_b200 import ablmc, capi
+
+pytestmark = pytest.mark.gpu
+
+Ig = ablmc.Integrator
+
+
+def make_problem(d, qoi=None):
+    mp = ablmc.ModelParams(**{k: d[k] for k in ("kappa_sigma", "kappa_tau", "u_star", "H",
+                                                  "eps_reg", "x_ref", "noise_scale")})
+    if qoi is None:
+        kind = ablmc.QoIKind(d.get("qoi_kind", 0))
+        qoi = ablmc.QoISpec(kind=kind, bin_edges=d.get("edges", []))
+    return ablmc.Problem.make(mp, Ig(d["integrator"]), qoi, d["x0"], d["u0"], d["T"], d["m0"],
+                              d["seed"], ablmc.SampleOptions(signs_on=bool(d["signs_on"])))
+
+
+def close(a, b, rel, ab):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    return np.all((np.abs(a - b) <= rel * np.abs(b)) | (np.abs(a - b) <= ab))
+
+
+def stream_xi(seed, level, first, count, M):
+    """The reference stream's normals (orc_normal_at is pinned bit-exact to
+    NoiseStream::normal_at by tests/test_oracle.py)."""
+    return np.array([O.orc_normals(seed, level, first + i, 0, M) for i in range(count)])
+
+
+# ------------------------------------------------------------------ noise
+def test_device_normals_vs_reference(ref_vectors):
+    worst = 0.0
+    for s in ref_vectors["normals"]:
+        z = ablmc.normals(s["seed"], s["level"], s["idx"], s["k0"], len(s["z"]))
+        want = np.array([fx(v) for v in s["z"]])
+        assert close(z, want, 1e-13, 1e-15)
+        worst = max(worst, float(np.max(np.abs(z - want) / np.abs(want))))
+    print(f"max rel deviation of device Box-Muller normals: {worst:.3e}")
+
+
+# ------------------------------------------------------------- oracle mode
+@pytest.mark.parametrize("case_idx", range(16))
+def test_pair_states_oracle_mode(ref_vectors, case_idx):
+    case = ref_vectors["pairs"][case_idx]
+    d = case["problem"]
+    pr = make_problem(d)
+    level, first = case["level"], case["first"]
+    count = len(case["states"])
+    M = d["m0"] << level
+    xi = stream_xi(d["seed"], level, first, count, M)
+    got = ablmc.simulate_pairs(pr, level, first, count, xi=xi)
+    want = case["states"]
+    ok = np.array([s[4] for s in want], bool)
+    assert np.array_equal(got["fok"].astype(bool), ok), case["name"]
+    g = got[ok]
+    w = [s for s in want if s[4]]
+    wx = np.array([[fx(s[0]), fx(s[1]), fx(s[5]), fx(s[6])] for s in w]).reshape(-1, 4)
+    gx = np.stack([g["fx"], g["fu"], g["cx"], g["cu"]], axis=1)
+    if d["integrator"] == 0:  # SE: no transcendental -> bit-identical
+        assert np.array_equal(gx, wx), case["name"]
+    else:
+        assert close(gx, wx, 1e-12, 1e-13), (case["name"], np.max(np.abs(gx - wx)))
+    assert [(s[2], s[3], s[7], s[8]) for s in w] == list(
+        zip(g["fpar"].tolist(), g["fn"].tolist(), g["cpar"].tolist(), g["cn"].tolist()))
+
+
+@pytest.mark.parametrize("case_idx", range(16))
+def test_pair_states_philox(ref_vectors, case_idx):
+    case = ref_vectors["pairs"][case_idx]
+    d = case["problem"]
+    pr = make_problem(d)
+    count = len(case["states"])
+    got = ablmc.simulate_pairs(pr, case["level"], case["first"], count)
+    want = case["states"]
+    ok = np.array([s[4] for s in want], bool)
+    assert np.array_equal(got["fok"].astype(bool), ok), case["name"]
+    w = [s for s in want if s[4]]
+    g = got[ok]
+    wx = np.array([[fx(s[0]), fx(s[1]), fx(s[5]), fx(s[6])] for s in w]).reshape(-1, 4)
+    gx = np.stack([g["fx"], g["fu"], g["cx"], g["cu"]], axis=1)
+    assert close(gx, wx, 1e-10, 1e-12), (case["name"], np.max(np.abs(gx - wx)))
+    assert [(s[2], s[3], s[7], s[8]) for s in w] == list(
+        zip(g["fpar"].tolist(), g["fn"].tolist(), g["cpar"].tolist(), g["cn"].tolist()))
+
+
+def test_survey_pair_kat():
+    # simulate_pair(se, defaults, 0.5, 0.1, T=1, M=8, NoiseStream(42, 3, idx))
+    pr = ablmc.Problem.make(ablmc.ModelParams(), Ig.se, ablmc.QoISpec(), 0.5, 0.1, 1.0, 1, 42)
+    s = ablmc.simulate_pairs(pr, 3, 0, 1)[0]
+    assert close([s["fx"], s["fu"], s["cx"], s["cu"]],
+                 [0.64579372369248766, 0.15921842792480534, 0.66134408294389468,
+                  0.15499307057678519], 1e-12, 0)
+    s = ablmc.simulate_pairs(pr, 3, 12345, 1)[0]
+    assert close([s["fx"], s["fu"], s["cx"], s["cu"]],
+                 [0.55708901811423728, 0.15391445097418696, 0.57230845534799446,
+                  0.15126588419736006], 1e-12, 0)
+
+
+@pytest.mark.parametrize("case_idx", range(6))
+def test_path_states(ref_vectors, case_idx):
+    case = ref_vectors["paths"][case_idx]
+    d = case["problem"]
+    pr = make_problem(d)
+    n = len(case["states"])
+    want = np.array([[fx(s[0]), fx(s[1])] for s in case["states"]])
+    for xi in (None, "stream"):
+        x = None
+        if xi:
+            x = stream_xi(d["seed"], case["stream_level"], case["first"], n, case["M"])
+        got = ablmc.simulate_paths(pr, case["M"], case["first"], n, case["stream_level"], xi=x)
+        assert got["ok"].all()
+        gx = np.stack([got["x"], got["u"]], axis=1)
+        if xi and d["integrator"] == 0:
+            assert np.array_equal(gx, want)
+        else:
+            assert close(gx, want, 1e-10 if xi is None else 1e-12, 1e-13)
+        assert got["parity"].tolist() == [s[2] for s in case["states"]]
+
+
+def test_oracle_mode_arbitrary_xi_heavy_reflection():
+    """Scaled normals drive many multi-wall reflections; GPU == C oracle."""
+    rng = np.random.default_rng(3)
+    mp = ablmc.ModelParams(u_star=1.0)
+    for ig in (Ig.se, Ig.gl, Ig.baoab):
+        pr = ablmc.Problem.make(mp, ig, ablmc.QoISpec(), 0.5, 0.0, 2.0, 16, 0)
+        level, n = 5, 64
+        M = 16 << level
+        xi = rng.normal(size=(n, M)) * 2.0
+        got = ablmc.simulate_pairs(pr, level, 0, n, xi=xi)
+        p = O.default_params(u_star=1.0)
+        for i in range(n):
+            rc, f, c = O.orc_pair(int(ig), p, 0.5, 0.0, 2.0, M, 0, level, i, xi=xi[i])
+            assert (rc == 0) == bool(got["fok"][i])
+            if rc == 0:
+                assert (got["fpar"][i], got["fn"][i], got["cpar"][i], got["cn"][i]) == (
+                    f.parity, f.n_refl, c.parity, c.n_refl)
+                v = [got["fx"][i], got["fu"][i], got["cx"][i], got["cu"][i]]
+                if ig == Ig.se:
+                    assert v == [f.x, f.u, c.x, c.u]
+                else:
+                    assert close(v, [f.x, f.u, c.x, c.u], 1e-12, 1e-13)
+        assert got["fn"].sum() > 50
+
+
+# -------------------------------------------------------- level sums
+@pytest.mark.parametrize("case_idx", range(36))
+def test_accumulate_vs_reference(ref_vectors, case_idx):
+    case = ref_vectors["accumulate"][case_idx]
+    d = case["problem"]
+    pr = make_problem(d)
+    dim = len(case["sum_y"])
+    acc = ablmc.LevelStats().init(case["level"], pr.h_level(case["level"]), dim)
+    ablmc.accumulate_samples(acc, case["first"], case["count"], pr, case["level"])
+    assert (acc.n, acc.failed, acc.cost_steps) == (case["n"], case["failed"], case["cost_steps"])
+    assert close(acc.sum_y, [fx(v) for v in case["sum_y"]], 1e-11, 1e-12)
+    assert close(acc.sum_y2, [fx(v) for v in case["sum_y2"]], 1e-11, 1e-12)
+
+
+def test_failures_counted_like_reference(ref_vectors):
+    case = next(c for c in ref_vectors["pairs"] if c["name"] == "se_unstable_failures")
+    d = case["problem"]
+    pr = make_problem(d)
+    n = len(case["states"])
+    want_failed = sum(1 - s[4] for s in case["states"])
+    acc = ablmc.LevelStats().init(1, pr.h_level(1), 1)
+    ablmc.accumulate_samples(acc, 0, n, pr, 1)
+    assert acc.failed == want_failed > 0
+    assert acc.n == n - want_failed
+    assert acc.cost_steps == acc.n * (4 + 2)  # failed samples contribute 0 steps
+    with pytest.raises(ablmc.SampleFailureError):
+        ablmc.check_failure_budget(acc)
+
+
+def test_constant_qoi_difference_is_zero():
+    # test_coupling.cpp:111-127
+    q = ablmc.QoISpec(kind=ablmc.QoIKind.binned_field, bin_edges=[0.0, 1.0])
+    for ig in Ig:
+        pr = ablmc.Problem.make(ablmc.ModelParams(), ig, q, 0.05, 0.1, 1.0, 40, 1)
+        acc = ablmc.LevelStats().init(2, pr.h_level(2), 1)
+        ablmc.accumulate_samples(acc, 7, 1, pr, 2)
+        assert acc.n == 1 and acc.cost_steps == 160 + 80 and acc.sum_y[0] == 0.0
+        acc = ablmc.LevelStats().init(2, pr.h_level(2), 1)
+        ablmc.accumulate_samples(acc, 0, 5000, pr, 2)
+        assert acc.sum_y[0] == 0.0 and acc.sum_y2[0] == 0.0
+
+
+def test_binned_64_and_indicators_vs_oracle():
+    edges = ablmc.equidistant_edges(64, 1.0)
+    qs = [ablmc.QoISpec(kind=ablmc.QoIKind.binned_field, bin_edges=edges),
+          ablmc.QoISpec(kind=ablmc.QoIKind.smoothed_indicator),
+          ablmc.QoISpec(kind=ablmc.QoIKind.raw_indicator)]
+    for q in qs:
+        for level in (0, 2):
+            pr = ablmc.Problem.make(ablmc.ModelParams(), Ig.gl, q, 0.01, 0.1, 1.0, 10, 4)
+            acc = ablmc.LevelStats().init(level, pr.h_level(level), q.size())
+            ablmc.accumulate_samples(acc, 11, 6000, pr, level)
+            ref = O.Stats(q.size())
+            assert O.orc().orc_accumulate_samples(C.byref(pr._c), level, 11, 6000,
+                                                  C.byref(ref.c)) == 0
+            assert (acc.n, acc.failed, acc.cost_steps) == (ref.n, ref.failed, ref.cost_steps)
+            assert close(acc.sum_y, ref.sum_y, 1e-11, 1e-11)
+            assert close(acc.sum_y2, ref.sum_y2, 1e-11, 1e-11)
+
+
+# ---------------------------------------------- determinism / partitioning
+def test_deterministic_and_add_merge():
+    pr = ablmc.Problem.make(ablmc.ModelParams(), Ig.baoab, ablmc.QoISpec(), 0.05, 0.1, 1.0, 4, 9)
+    a = ablmc.LevelStats().init(3, pr.h_level(3), 1)
+    b = ablmc.LevelStats().init(3, pr.h_level(3), 1)
+    ablmc.accumulate_samples(a, 0, 300_000, pr, 3)
+    ablmc.accumulate_samples(b, 0, 300_000, pr, 3)
+    assert a.sum_y[0] == b.sum_y[0] and a.sum_y2[0] == b.sum_y2[0] and a.n == b.n
+    # continuing indices (first = attempts()) adds exactly the next samples
+    c = ablmc.LevelStats().init(3, pr.h_level(3), 1)
+    ablmc.accumulate_samples(c, 0, 100_000, pr, 3)
+    ablmc.accumulate_samples(c, c.attempts(), 200_000, pr, 3)
+    assert c.n == a.n and c.cost_steps == a.cost_steps
+    assert abs(c.sum_y[0] - a.sum_y[0]) <= 1e-12 * abs(a.sum_y[0])
+
+
+def test_superblock_sharding_is_bit_identical():
+    pr = ablmc.Problem.make(ablmc.ModelParams(), Ig.gl, ablmc.QoISpec(), 0.05, 0.1, 1.0, 2, 21)
+    count = 3 * capi.ABLMC_SUPERBLOCK + 12345  # ragged last super-block
+    one = ablmc.LevelStats().init(1, pr.h_level(1), 1)
+    ablmc.accumulate_samples(one, 17, count, pr, 1)
+    nsb = ablmc.num_superblocks(count)
+    assert nsb == 4
+    for split in ([0, 4], [0, 1, 4], [0, 2, 3, 4], [0, 1, 2, 3, 4]):
+        parts = [ablmc.accumulate_partials(pr, 1, 17, count, lo, hi)
+                 for lo, hi in zip(split[:-1], split[1:])]
+        sums = np.concatenate([p[0] for p in parts])
+        cnts = np.concatenate([p[1] for p in parts])
+        acc = ablmc.LevelStats().init(1, pr.h_level(1), 1)
+        ablmc.merge_partials(acc, pr, 1, sums, cnts)
+        assert acc.sum_y[0] == one.sum_y[0] and acc.sum_y2[0] == one.sum_y2[0]
+        assert (acc.n, acc.failed, acc.cost_steps) == (one.n, one.failed, one.cost_steps)
+
+
+def test_device_resident_result_matches_host_path():
+    pr = ablmc.Problem.make(ablmc.ModelParams(), Ig.se, ablmc.QoISpec(), 0.5, 0.1, 1.0, 1, 42)
+    lib = ablmc.lib()
+    assert lib.ablmc_accumulate_device(C.byref(pr._c), 6, 0, 1_000_000) == 0
+    dev = ablmc.LevelStats().init(6, pr.h_level(6), 1)
+    v = dev._view()
+    assert lib.ablmc_fetch_device_result(C.byref(pr._c), 6, C.byref(v)) == 0
+    dev._take(v)
+    host = ablmc.LevelStats().init(6, pr.h_level(6), 1)
+    ablmc.accumulate_samples(host, 0, 1_000_000, pr, 6)
+    assert dev.sum_y[0] == host.sum_y[0] and dev.n == host.n and dev.cost_steps == host.cost_steps
+
+
+def test_edge_cases():
+    pr = ablmc.Problem.make(ablmc.ModelParams(), Ig.gl, ablmc.QoISpec(), 0.05, 0.1, 1.0, 40, 5)
+    acc = ablmc.LevelStats().init(1, pr.h_level(1), 1)
+    ablmc.accumulate_samples(acc, 0, 1, pr, 1)
+    assert acc.n == 1
+    # huge first index (64-bit counter words) vs oracle
+    for first in (2**40 + 1, 2**62):
+        acc = ablmc.LevelStats().init(1, pr.h_level(1), 1)
+        ablmc.accumulate_samples(acc, first, 4097, pr, 1)
+        ref = O.Stats(1)
+        assert O.orc().orc_accumulate_samples(C.byref(pr._c), 1, first, 4097, C.byref(ref.c)) == 0
+        assert acc.n == ref.n and close(acc.sum_y, ref.sum_y, 1e-11, 1e-14)
+    # odd path length (last Philox block half used) through accumulate_paths
+    acc = ablmc.LevelStats().init(0, 1 / 7, 1)
+    ablmc.accumulate_paths(acc, 3, 5000, pr, 7, 31)
+    ref = O.Stats(1)
+    assert O.orc().orc_accumulate_paths(C.byref(pr._c), 7, 31, 3, 5000, C.byref(ref.c)) == 0
+    assert acc.n == ref.n and acc.cost_steps == ref.cost_steps
+    assert close(acc.sum_y, ref.sum_y, 1e-11, 0)
+    with pytest.raises(ValueError):
+        ablmc.accumulate_samples(acc, 0, 10, pr, -1)
+
+
+# ------------------------------------------------------- statistics
+def test_level_statistics_vs_reference_same_streams():
+    """Config-2 analogue: reference profile, x0 = 0.5, u0 = 0.1,
+    M0 = 1, seed 42: GPU and reference see the same streams, so E[Y_l] and
+    Var[Y_l] agree to rounding, far inside 3 combined standard errors."""
+    R = O.ref()
+    if R is None:
+        pytest.skip("oracle/_ref not built")
+    for ig in Ig:
+        pr = ablmc.Problem.make(ablmc.ModelParams(), ig, ablmc.QoISpec(), 0.5, 0.1, 1.0, 1, 42)
+        for level in (1, 3, 6):
+            n = 100_000
+            g = ablmc.LevelStats().init(level, pr.h_level(level), 1)
+            ablmc.accumulate_samples(g, 0, n, pr, level)
+            r = O.Stats(1)
+            assert R.ref_accumulate_samples(C.byref(pr._c), level, 0, n, 8, C.byref(r.c), None) == 0
+            assert g.n == r.n and g.failed == r.failed
+            assert abs(g.sum_y[0] - r.sum_y[0]) <= 1e-10 * abs(r.sum_y[0]) + 1e-12
+            assert abs(g.sum_y2[0] - r.sum_y2[0]) <= 1e-10 * abs(r.sum_y2[0])
+
+
+def test_mlmc_estimate_agrees_with_reference_independent_seeds():
+    """run_mlmc on the device vs the reference's run_mlmc with a different
+    seed: estimates within 3 combined standard errors + both bias bounds."""
+    R = O.ref()
+    if R is None:
+        pytest.skip("oracle/_ref not built")
+    eps = 1e-3
+    pr = ablmc.Problem.make(ablmc.ModelParams(), Ig.gl, ablmc.QoISpec(), 0.05, 0.1, 1.0, 40, 555)
+    g = ablmc.run_mlmc(pr, eps)
+    pr2 = pr.with_seed(556)
+    o = capi.MlmcOptionsC()
+    ablmc.lib().ablmc_mlmc_options_defaults(C.byref(o))
+    r = capi.RunResultC()
+    assert R.ref_run_mlmc(C.byref(pr2._c), eps, C.byref(o), 16, C.byref(r)) == 0
+    se = (g.stat_error[0] ** 2 + r.stat_error ** 2) ** 0.5
+    assert abs(g.estimate[0] - r.estimate) <= 3 * se + g.bias_estimate + r.bias_estimate
+    assert g.stat_error[0] ** 2 <= 0.5 * eps * eps * 1.0001  # completion contract
+    assert g.failed_samples == 0 and g.levels_used >= 1
