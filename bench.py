@@ -198,7 +198,10 @@ def run_b200(a):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ablmc.init(local)
-    stream = torch.cuda.current_stream()
+    # A dedicated (non-default) stream shared by torch and the library, so the
+    # CUDA events below bracket exactly the library's kernels.
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     ablmc.set_stream(stream.cuda_stream)
     lib = ablmc.lib()
 
@@ -246,6 +249,9 @@ def run_b200(a):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(a.steps)]
     launches = 0
+    k1_ms, k1_n = C.c_double(), C.c_int64()
+    lib.ablmc_level_kernel_times(C.byref(k1_ms), C.byref(k1_n))  # reset
+    lib.ablmc_set_profiling(1)
     with ClockSampler(local) as clk:
         for i in range(a.steps):
             flush.zero_()  # L2 flush between timed iterations (outside the events)
@@ -254,8 +260,13 @@ def run_b200(a):
             launches += device_step()
             ev[i][1].record(stream)
         barrier()
+    lib.ablmc_set_profiling(0)
+    lib.ablmc_level_kernel_times(C.byref(k1_ms), C.byref(k1_n))
     ms = [s.elapsed_time(e) for s, e in ev]
     total_ms = max_over_ranks(sum(ms))
+    k1_avg_ms = k1_ms.value / max(1, k1_n.value)
+    k1_share = k1_ms.value / sum(ms)
+    steps_per_launch = N * Mf * a.steps / max(1, k1_n.value)
     ms_per_step = total_ms / a.steps
     value = world * N * Mf / (ms_per_step * 1e-3)
 
@@ -269,8 +280,14 @@ def run_b200(a):
     # (N paths in one chunk of 2^25 -> one K1 launch dominates the step)
     fp64_rate = C.c_double()
     ablmc._check(lib.ablmc_probe_fp64_rate(C.byref(fp64_rate)))
-    achieved = value / world * W_ALG[ig]  # per-GPU algorithmic FP64 lane-ops/s
+    # dominant kernel (K1, the fused level sampler): algorithmic FP64-pipe ops
+    # per launch / its average launch duration (CUDA events on its stream)
+    achieved = steps_per_launch * W_ALG[ig] / (k1_avg_ms * 1e-3)
     peak = fp64_rate.value
+    traffic = None  # DRAM bytes per K1 launch, scaled from the committed ncu capture
+    tp = ROOT / "profiles" / "k1_traffic.json"
+    if tp.exists():
+        traffic = json.loads(tp.read_text())["dram_bytes_per_path_step"] * steps_per_launch
 
     # ---- e2e: public API, host LevelStats in/out, sharded + gathered
     e2e_times = []
@@ -320,10 +337,14 @@ def run_b200(a):
         "gpu_launches": int(launches),
         "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12,
                      "unit": "FP64 Tops/s (pipe lane-ops)", "frac": achieved / peak,
-                     "traffic": None,
-                     "note": f"achieved = path-steps/s/GPU x W_alg={W_ALG[ig]:.0f} FP64-pipe ops per "
-                             "coupled fine path-step (SURVEY.md 8(d)); peak = DFMA probe measured "
-                             "in this run (MEASURED_PEAKS.json has no FP64 entry)"},
+                     "traffic": traffic,
+                     "kernel": "k_level (K1, fused coupled level sampler)",
+                     "kernel_avg_ms": k1_avg_ms, "kernel_share_of_step": k1_share,
+                     "path_steps_per_launch": steps_per_launch,
+                     "note": f"achieved = coupled fine path-steps per K1 launch x W_alg="
+                             f"{W_ALG[ig]:.0f} FP64-pipe ops per path-step (SURVEY.md 8(d)) / K1 "
+                             "launch time; peak = DFMA probe measured in this run "
+                             "(MEASURED_PEAKS.json has no FP64 entry)"},
         "clocks": clk.summary(),
         "estimate": {"mean_y": acc.mean(), "n": acc.n, "failed": acc.failed},
     }

@@ -76,7 +76,8 @@ def init(device: int = -1) -> None:
 
 
 def set_stream(cuda_stream: int | None) -> None:
-    """Launch on this cudaStream_t (e.g. ``torch.cuda.current_stream().cuda_stream``)."""
+    """Launch on this cudaStream_t (e.g. ``torch.cuda.Stream().cuda_stream``).
+    0/None selects the library's own stream (NOT the legacy default stream)."""
     lib().ablmc_set_stream(C.c_void_p(cuda_stream) if cuda_stream else None)
 
 

@@ -116,6 +116,8 @@ SIGNATURES = {
     "ablmc_fetch_device_result": (C.c_int, [P(ProblemC), C.c_int, P(LevelStatsC)]),
     "ablmc_copy_device_result": (C.c_int, [C.c_void_p, C.c_void_p]),
     "ablmc_last_launch_count": (C.c_int64, []),
+    "ablmc_set_profiling": (C.c_int, [C.c_int]),
+    "ablmc_level_kernel_times": (C.c_int, [P(C.c_double), P(C.c_int64)]),
     "ablmc_probe_fp64_rate": (C.c_int, [P(C.c_double)]),
     "ablmc_pair_states": (C.c_int, [P(ProblemC), C.c_int, C.c_int64, C.c_int64, P(C.c_double),
                                     P(PairStateC)]),
