@@ -27,6 +27,7 @@ struct KernelArgs {
   int signs_on;
   int random_u0;
   int qoi_kind;
+  int fast;                 // 1: tame parameters, fast div/sqrt with IEEE recompute on a miss
   int dim;
   double qa, qb, delta;
   int poly_n;               // r + 2 coefficients
@@ -55,3 +56,8 @@ cudaError_t launch_normals(uint32_t k0, uint32_t k1, uint64_t idx, uint64_t ksta
                            double* out, cudaStream_t st);
 // DFMA throughput probe (FP64 lane-ops/s), see ablmc_probe_fp64_rate.
 cudaError_t probe_fp64(cudaStream_t st, double* lane_ops_per_s);
+// Device self-test of the fast IEEE div/sqrt and the Box-Muller libm kernels:
+// out[0..8] = {div checked, div mismatches where ok, div misses, sqrt checked,
+// sqrt mismatches where ok, sqrt misses, max ulp log_unit vs libdevice log,
+// max |sin - libdevice sin| and |cos - ...| in units of 0.01 * 2^-53}.
+cudaError_t launch_selftest(int64_t n, uint64_t seed, unsigned long long* d_out, cudaStream_t st);
