@@ -141,7 +141,8 @@ def load(path: os.PathLike | str | None = None) -> C.CDLL:
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    # ABLMC_LIB: an alternative in-tree build of the same library (A/B tuning runs)
+    p = Path(path) if path else Path(os.environ.get("ABLMC_LIB") or LIB_PATH)
     if not p.exists():
         raise ImportError(
             f"{p} is missing: build it with `python -m paper_1612_07717_b200.build` "

@@ -11,6 +11,15 @@
 #define ABLMC_TILES_PER_BLOCK 16       // 16 * 256 = 4096 = reference block_size (stats.hpp:100)
 #define ABLMC_BLOCKS_PER_SUPER 1024    // 1024 * 4096 = 2^22 = ABLMC_SUPERBLOCK
 #define ABLMC_MAX_POLY 14
+#ifndef ABLMC_MINB_SE
+#define ABLMC_MINB_SE 4
+#endif
+#ifndef ABLMC_MINB_GL
+#define ABLMC_MINB_GL 3
+#endif
+#ifndef ABLMC_MINB_BAOAB
+#define ABLMC_MINB_BAOAB 2
+#endif
 
 // Everything one launch needs, passed by value (kernel-parameter constant bank).
 struct KernelArgs {
