@@ -71,7 +71,30 @@ def build_oracle() -> None:
         raise RuntimeError(f"oracle build failed:\n{r.stdout}\n{r.stderr}")
 
 
+REF_INCLUDE = Path("/root/reference/proj/include")
+DEMO = ROOT / "integration" / "adapter_demo"
+
+
+def build_integration_demo() -> None:
+    """integration/adapter_demo: the reference's own code calling this library
+    through integration/ablmc_b200_adapter.hpp (needs the reference headers,
+    so it is built here only; the binary travels to the GPU box)."""
+    if not REF_INCLUDE.is_dir():
+        return
+    src = ROOT / "integration" / "adapter_demo.cpp"
+    deps = [src, ROOT / "integration" / "ablmc_b200_adapter.hpp", LIB]
+    if not _stale(DEMO, deps):
+        return
+    cmd = ["g++", "-std=gnu++20", "-O2", "-pthread", f"-I{REF_INCLUDE}", f"-I{ROOT / 'include'}",
+           f"-I{ROOT / 'integration'}", str(src), "-o", str(DEMO), f"-L{PKG}", "-l:libablmc_b200.so",
+           "-Wl,-rpath,$ORIGIN/../paper_1612_07717_b200"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"adapter demo build failed:\n{r.stdout}\n{r.stderr}")
+
+
 if __name__ == "__main__":
     lib = build(verbose=True, force="--force" in sys.argv)
     build_oracle()
+    build_integration_demo()
     print(lib)

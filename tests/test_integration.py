@@ -1,0 +1,37 @@
+"""The reference's own C++ (unmodified headers) calling this library through
+integration/ablmc_b200_adapter.hpp — the binding INTEGRATION.md describes.
+The demo binary is built by __graft_entry__.build() where /root/reference
+exists and travels to the GPU box."""
+import subprocess
+from pathlib import Path
+
+import pytest
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+DEMO = ROOT / "integration" / "adapter_demo"
+
+needs_demo = pytest.mark.skipif(not DEMO.exists(), reason="adapter demo not built")
+
+
+@needs_demo
+def test_adapter_fails_loudly_without_gpu():
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    r = subprocess.run([str(DEMO), "100"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 3 and "device error" in r.stdout
+
+
+@needs_demo
+@pytest.mark.gpu
+def test_adapter_matches_reference_accumulate():
+    r = subprocess.run([str(DEMO), "20000"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    lines = [l.split() for l in r.stdout.splitlines() if l.startswith("level")]
+    assert len(lines) == 4
+    for t in lines:
+        g_y, g_y2, g_n, g_c = float(t[3]), float(t[4]), int(t[5]), int(t[6])
+        c_y, c_y2, c_n, c_c = float(t[8]), float(t[9]), int(t[10]), int(t[11])
+        assert (g_n, g_c) == (c_n, c_c)
+        assert abs(g_y - c_y) <= 1e-11 * abs(c_y) + 1e-13
+        assert abs(g_y2 - c_y2) <= 1e-11 * abs(c_y2)
