@@ -47,6 +47,10 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target wall time of the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the per-integrator lines and the MLMC time-to-eps sweep")
+    ap.add_argument("--mlmc-eps", default="1e-4,3e-5,1e-5,3e-6",
+                    help="config-3 tolerances (nondimensional: eps[m] / 1000 m)")
     return ap.parse_args()
 
 
@@ -180,6 +184,70 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
                 "samples": len(self.samples)}
+
+
+# ------------------------------------------------------- extra measurements
+def per_integrator(a, lib, stream, peak):
+    """Level-10 coupled throughput of all three integrators (2^23 paths, one
+    warm-up + 2 timed accumulate calls each, CUDA events on the stream)."""
+    import torch
+    out = {}
+    n = 1 << 23
+    for ig in (0, 1, 2):
+        pr = problem_c(ig)
+        pc = C.byref(pr._c)
+        lib.ablmc_accumulate_device(pc, a.level, 0, n)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        s.record(stream)
+        for _ in range(2):
+            lib.ablmc_accumulate_device(pc, a.level, 0, n)
+        e.record(stream)
+        torch.cuda.synchronize()
+        rate = 2 * n * (1 << a.level) / (s.elapsed_time(e) * 1e-3)
+        out[IG_NAME[ig]] = {"path_steps_per_s": rate, "W_alg": W_ALG[ig],
+                            "roofline_frac": rate * W_ALG[ig] / peak, "paths": n}
+    return out
+
+
+def mlmc_sweep(a):
+    """BASELINE config 3: full MLMC driver (reference run_mlmc semantics,
+    estimators.hpp:284-397) on the reference profile, BAOAB, x0 = 0.5,
+    u0 = 0.1, T = 1, M0 = 1, mean position, for each tolerance; wall time of
+    the whole driver (host allocation loop + device level sampler)."""
+    from paper_1612_07717_b200 import ablmc, capi
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib as O
+    R = O.ref()
+    threads = host_threads()
+    res = {}
+    pr = problem_c(2)
+    for eps in [float(e) for e in a.mlmc_eps.split(",") if e]:
+        t0 = time.perf_counter()
+        r = ablmc.run_mlmc(pr, eps)
+        t = time.perf_counter() - t0
+        row = {"seconds": t, "estimate": r.estimate[0], "stat_error": r.stat_error[0],
+               "bias_estimate": r.bias_estimate, "levels": r.levels_used,
+               "N_l": [st.n for st in r.level_stats], "total_cost_steps": r.total_cost_steps,
+               "eps_m": eps * 1000.0}
+        # StMC at the finest resolved level M0 2^L (estimators.hpp:230-269)
+        t0 = time.perf_counter()
+        s = ablmc.run_stmc(pr, 1 << r.levels_used, eps)
+        row["stmc_seconds"] = time.perf_counter() - t0
+        row["stmc_cost_steps"] = s.total_cost_steps
+        # the reference's own CPU run_mlmc, all host threads, bounded to eps >= 1e-5
+        if R is not None and eps >= 1e-5:
+            o = capi.MlmcOptionsC()
+            ablmc.lib().ablmc_mlmc_options_defaults(C.byref(o))
+            rr = capi.RunResultC()
+            t0 = time.perf_counter()
+            rc = R.ref_run_mlmc(C.byref(pr._c), eps, C.byref(o), threads, C.byref(rr))
+            if rc == 0:
+                row["reference_cpu_seconds"] = time.perf_counter() - t0
+                row["reference_cpu_estimate"] = rr.estimate
+                row["reference_cpu_threads"] = threads
+        res[f"{eps:g}"] = row
+    return res
 
 
 # ---------------------------------------------------------------- B200 arm
@@ -348,6 +416,9 @@ def run_b200(a):
         "clocks": clk.summary(),
         "estimate": {"mean_y": acc.mean(), "n": acc.n, "failed": acc.failed},
     }
+    if not a.no_extras and world == 1:
+        line["per_integrator"] = per_integrator(a, lib, stream, fp64_rate.value)
+        line["mlmc_time_to_eps"] = mlmc_sweep(a)
     if not a.no_cpu_baseline and world == 1:
         threads = host_threads()
         rate, n_cpu, secs = reference_sample(ig, level, a.cpu_seconds, threads)
