@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target wall time of the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="use the NCCL process group and collectives even at world size 1")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the per-integrator lines and the MLMC time-to-eps sweep")
     ap.add_argument("--mlmc-eps", default="1e-4,3e-5,1e-5,3e-6",
@@ -263,7 +265,8 @@ def run_b200(a):
     if world != a.gpus:
         raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
-    if world > 1:
+    dist_on = world > 1 or a.force_dist
+    if dist_on:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ablmc.init(local)
     # A dedicated (non-default) stream shared by torch and the library, so the
@@ -282,12 +285,12 @@ def run_b200(a):
     pc = C.byref(pr._c)
 
     def barrier():
-        if world > 1:
+        if dist_on:
             dist.barrier()
         torch.cuda.synchronize()
 
     def max_over_ranks(x: float) -> float:
-        if world == 1:
+        if not dist_on:
             return x
         t = torch.tensor([x], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -304,7 +307,7 @@ def run_b200(a):
         if rc:
             ablmc._check(rc)
         launches = lib.ablmc_last_launch_count()
-        if world > 1:  # one collective per step: all-gather of the per-rank moments
+        if dist_on:  # one collective per step: all-gather of the per-rank moments
             lib.ablmc_copy_device_result(C.c_void_p(res_s.data_ptr()), C.c_void_p(res_c.data_ptr()))
             dist.all_gather_into_tensor(gat_s, res_s)
             dist.all_gather_into_tensor(gat_c, res_c)
@@ -364,7 +367,7 @@ def run_b200(a):
         barrier()
         t0 = time.perf_counter()
         sums, cnts = ablmc.accumulate_partials(pr, level, first, N, 0, n_sb)
-        if world > 1:
+        if dist_on:
             t_s = torch.from_numpy(sums).cuda()
             t_c = torch.from_numpy(cnts).cuda()
             g_s = [torch.empty_like(t_s) for _ in range(world)]
@@ -384,7 +387,7 @@ def run_b200(a):
     d2h = n_sb * (2 * 1 + 2) * 8  # super-block partials
 
     if rank != 0:
-        if world > 1:
+        if dist_on:
             dist.barrier()
             dist.destroy_process_group()
         return
@@ -427,7 +430,7 @@ def run_b200(a):
                                 "sample": f"{n_cpu} coupled paths x {Mf} fine steps in {secs:.1f} s, "
                                           f"reference accumulate_samples, {threads} threads"}
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_on:
         dist.barrier()
         dist.destroy_process_group()
 
