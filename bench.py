@@ -360,31 +360,29 @@ def run_b200(a):
     if tp.exists():
         traffic = json.loads(tp.read_text())["dram_bytes_per_path_step"] * steps_per_launch
 
-    # ---- e2e: public API, host LevelStats in/out, sharded + gathered
+    # ---- e2e: the public API call a user makes (accumulate_samples into a
+    # host LevelStats) over the whole job's index range [0, world N); with
+    # several ranks the library's collective splits it by super-blocks
+    # (rank r gets [r N, (r+1) N)) and all-gathers the partials once per call.
+    if dist_on:
+        from paper_1612_07717_b200.sharding import disable_collective, enable_collective
+        enable_collective()
     e2e_times = []
     n_sb = ablmc.num_superblocks(N)
     for i in range(a.warmup + a.steps):
         barrier()
         t0 = time.perf_counter()
-        sums, cnts = ablmc.accumulate_partials(pr, level, first, N, 0, n_sb)
-        if dist_on:
-            t_s = torch.from_numpy(sums).cuda()
-            t_c = torch.from_numpy(cnts).cuda()
-            g_s = [torch.empty_like(t_s) for _ in range(world)]
-            g_c = [torch.empty_like(t_c) for _ in range(world)]
-            dist.all_gather(g_s, t_s)
-            dist.all_gather(g_c, t_c)
-            sums = torch.cat(g_s).cpu().numpy()
-            cnts = torch.cat(g_c).cpu().numpy()
         e2e_acc = ablmc.LevelStats().init(level, pr.h_level(level), 1)
-        ablmc.merge_partials(e2e_acc, pr, level, sums, cnts)
+        ablmc.accumulate_samples(e2e_acc, 0, world * N, pr, level)
         t1 = time.perf_counter()
         if i >= a.warmup:
             e2e_times.append(t1 - t0)
+    if dist_on:
+        disable_collective()
     e2e_t = max_over_ranks(statistics.mean(e2e_times))
     e2e_value = world * N * Mf / e2e_t
     h2d = C.sizeof(pr._c)  # the problem descriptor (kernel parameters) per call
-    d2h = n_sb * (2 * 1 + 2) * 8  # super-block partials
+    d2h = n_sb * (2 * 1 + 2) * 8  # this rank's super-block partials
 
     if rank != 0:
         if dist_on:

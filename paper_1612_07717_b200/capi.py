@@ -89,8 +89,10 @@ class DecayRowC(C.Structure):
 
 
 P = C.POINTER
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, P(C.c_double), C.c_int64, P(C.c_double))
 # name -> (restype, argtypes): every symbol include/ablmc_b200.h declares.
 SIGNATURES = {
+    "ablmc_set_collective": (C.c_int, [C.c_int, C.c_int, ALLGATHER_FN, C.c_void_p]),
     "ablmc_abi_version": (C.c_int, []),
     "ablmc_init": (C.c_int, [C.c_int]),
     "ablmc_finalize": (C.c_int, []),

@@ -18,6 +18,46 @@ import numpy as np
 from . import ablmc, capi
 
 
+_collective_keepalive = None
+
+
+def enable_collective(group=None) -> None:
+    """Route every accumulate call of the library (and so every iteration of
+    run_mlmc / run_stmc / decay_sweep) through this process group: each rank
+    computes its contiguous super-block range and ONE all-gather per call
+    (NCCL over NVLink for an "nccl" group; gloo on host for a CPU group)
+    exchanges the partials (ablmc_set_collective in include/ablmc_b200.h)."""
+    import torch
+    import torch.distributed as dist
+
+    global _collective_keepalive
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    nccl = dist.get_backend(group) == "nccl"
+    dev = torch.device("cuda", torch.cuda.current_device()) if nccl else torch.device("cpu")
+
+    def allgather(ctx, send, count, recv):
+        try:
+            src = np.ctypeslib.as_array(send, (count,))
+            t = torch.from_numpy(src.copy()).to(dev)
+            outs = [torch.empty_like(t) for _ in range(world)]
+            dist.all_gather(outs, t, group=group)
+            np.ctypeslib.as_array(recv, (world * count,))[:] = torch.cat(outs).cpu().numpy()
+            return 0
+        except Exception:  # noqa: BLE001 - reported to the C side as a failed collective
+            return 1
+
+    cb = capi.ALLGATHER_FN(allgather)
+    _collective_keepalive = cb
+    ablmc._check(ablmc.lib().ablmc_set_collective(rank, world, cb, None))
+
+
+def disable_collective() -> None:
+    global _collective_keepalive
+    ablmc.lib().ablmc_set_collective(0, 1, capi.ALLGATHER_FN(), None)
+    _collective_keepalive = None
+
+
 def shard_superblocks(n_sb: int, rank: int, world: int) -> tuple[int, int]:
     """Contiguous, balanced super-block range [lo, hi) of `rank`."""
     base, extra = divmod(n_sb, world)
