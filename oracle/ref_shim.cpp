@@ -15,8 +15,10 @@
 #include <stdexcept>
 #include <string>
 
+#include "ablmc/config.hpp"
 #include "ablmc/coupling.hpp"
 #include "ablmc/estimators.hpp"
+#include "ablmc/output.hpp"
 #include "ablmc/integrators.hpp"
 #include "ablmc/model.hpp"
 #include "ablmc/noise.hpp"
@@ -287,7 +289,23 @@ int ref_decay_sweep(const ablmc_problem* prc, int l_min, int l_max, int64_t n, i
 }
 
 static void fill_result(const RunResult& r, ablmc_run_result* out) {
-  std::memset(out, 0, sizeof(*out) - 2 * sizeof(double*));
+  double* keep[4] = {out->est_vec, out->err_vec, out->level_sum_y_vec, out->level_sum_y2_vec};
+  std::memset(out, 0, sizeof(*out));
+  out->est_vec = keep[0];
+  out->err_vec = keep[1];
+  out->level_sum_y_vec = keep[2];
+  out->level_sum_y2_vec = keep[3];
+  for (const auto& w : r.warnings) {
+    if (w.rfind("Var[Y_1]", 0) == 0) out->warnings_mask |= 1;
+    if (w.rfind("sample allocation", 0) == 0) out->warnings_mask |= 2;
+  }
+  for (std::size_t l = 0; l < r.level_stats.size() && l < ABLMC_MAX_LEVELS; ++l) {
+    const LevelStats& st = r.level_stats[l];
+    for (std::size_t i = 0; i < st.dim; ++i) {
+      if (out->level_sum_y_vec) out->level_sum_y_vec[l * st.dim + i] = st.sum_y[i];
+      if (out->level_sum_y2_vec) out->level_sum_y2_vec[l * st.dim + i] = st.sum_y2[i];
+    }
+  }
   out->levels_used = r.levels_used;
   out->n_levels = int(r.level_stats.size());
   out->estimate = r.estimate.empty() ? 0.0 : r.estimate[0];
@@ -332,6 +350,138 @@ int ref_run_mlmc(const ablmc_problem* prc, double eps, const ablmc_mlmc_options*
       mo.bias_fit = &fit;
     }
     fill_result(run_mlmc(pr, eps, mo), out);
+  });
+}
+
+// ---------------------------------------------------------- output.hpp
+static RunConfig to_cfg(const ablmc_run_config& c) {
+  RunConfig k;
+  k.model = to_params(c.model);
+  k.method = c.method == 0 ? Method::stmc : Method::mlmc;
+  k.integrator = to_ig(c.integrator);
+  k.qoi_kind = static_cast<QoIKind>(c.qoi_kind);
+  k.qoi_a = c.qoi_a;
+  k.qoi_b = c.qoi_b;
+  k.qoi_r = c.qoi_r;
+  k.qoi_delta = c.qoi_delta;
+  k.qoi_bins = c.qoi_bins;
+  k.T = c.T;
+  k.m0 = c.m0;
+  k.eps = c.eps;
+  k.fixed_n = c.fixed_n;
+  k.seed = c.seed;
+  k.x0 = c.x0;
+  k.u0 = c.u0;
+  k.adaptive = c.adaptive != 0;
+  k.x_adapt = c.x_adapt;
+  k.coupling_signs = c.coupling_signs != 0;
+  k.workers = c.workers;
+  k.timings = c.timings != 0;
+  k.output_dir = c.output_dir ? c.output_dir : ".";
+  return k;
+}
+
+static RunResult to_res(const ablmc_run_result& r, int64_t dim) {
+  RunResult o;
+  for (int64_t i = 0; i < dim; ++i) {
+    o.estimate.push_back(r.est_vec ? r.est_vec[i] : r.estimate);
+    o.stat_error.push_back(r.err_vec ? r.err_vec[i] : r.stat_error);
+  }
+  o.bias_estimate = r.bias_estimate;
+  o.alpha = r.alpha;
+  o.c1 = r.c1;
+  o.levels_used = r.levels_used;
+  o.total_cost_steps = r.total_cost_steps;
+  o.pilot_cost_steps = r.pilot_cost_steps;
+  o.failed_samples = r.failed_samples;
+  o.wall_seconds = r.wall_seconds;
+  if (r.warnings_mask & 1)
+    o.warnings.push_back("Var[Y_1] >= Var[Y_0]/2: coarsest level M_0 is too coarse to pay off");
+  if (r.warnings_mask & 2) o.warnings.push_back("sample allocation did not converge in 64 rounds");
+  for (int l = 0; l < r.n_levels; ++l) {
+    LevelStats st;
+    st.init(l, r.level_h[l], std::size_t(dim));
+    for (int64_t i = 0; i < dim; ++i) {
+      st.sum_y[i] = r.level_sum_y_vec ? r.level_sum_y_vec[l * dim + i] : r.level_sum_y[l];
+      st.sum_y2[i] = r.level_sum_y2_vec ? r.level_sum_y2_vec[l * dim + i] : r.level_sum_y2[l];
+    }
+    st.n = r.level_n[l];
+    st.failed = r.level_failed[l];
+    st.cost_steps = r.level_cost[l];
+    o.level_stats.push_back(std::move(st));
+  }
+  return o;
+}
+
+static int64_t emit(const std::string& s, char* buf, int64_t cap) {
+  if (buf && cap > 0) {
+    const std::size_t n = std::min<std::size_t>(s.size(), std::size_t(cap - 1));
+    std::memcpy(buf, s.data(), n);
+    buf[n] = '\0';
+  }
+  return int64_t(s.size());
+}
+
+// exactly what write_result_json (output.hpp:213-219) writes
+int64_t ref_result_json(const ablmc_run_config* c, const ablmc_run_result* r, int64_t dim,
+                        char* buf, int64_t cap) {
+  OutputRecord rec;
+  rec.config = to_cfg(*c);
+  rec.result = to_res(*r, dim);
+  return emit(to_json(rec).dump(2) + "\n", buf, cap);
+}
+
+int64_t ref_variance_decay_csv(const ablmc_decay_row* rows, int n, char* buf, int64_t cap) {
+  std::vector<DecayRow> v;
+  for (int i = 0; i < n; ++i)
+    v.push_back({rows[i].level, rows[i].h, rows[i].var_y, rows[i].mean_y, rows[i].se_mean,
+                 rows[i].n, rows[i].cost_steps});
+  return emit(variance_decay_csv(v), buf, cap);
+}
+
+int64_t ref_cost_sweep_csv(const ablmc_cost_row* rows, int n, int timings, char* buf,
+                           int64_t cap) {
+  std::vector<CostRow> v;
+  for (int i = 0; i < n; ++i) {
+    CostRow r;
+    r.eps = rows[i].eps;
+    r.method = rows[i].method == 0 ? Method::stmc : Method::mlmc;
+    r.integrator = to_ig(rows[i].integrator);
+    r.cost_steps = rows[i].cost_steps;
+    r.wall_seconds = rows[i].wall_seconds;
+    r.estimate = rows[i].estimate;
+    r.stat_error = rows[i].stat_error;
+    v.push_back(r);
+  }
+  return emit(cost_sweep_csv(v, timings != 0), buf, cap);
+}
+
+int64_t ref_pdf_csv(const double* edges, int n_edges, const double* conc, const double* se,
+                    char* buf, int64_t cap) {
+  return emit(pdf_csv(std::span<const double>(edges, std::size_t(n_edges)),
+                      std::span<const double>(conc, std::size_t(n_edges - 1)),
+                      std::span<const double>(se, std::size_t(n_edges - 1))),
+              buf, cap);
+}
+
+int ref_cost_sweep(const ablmc_problem* prc, int method, const double* eps, int n_eps,
+                   double alpha, double c1, int workers, ablmc_cost_row* rows) {
+  return guarded([&] {
+    const Problem pr = to_problem(*prc);
+    BiasFit fit;
+    fit.alpha = alpha;
+    fit.c1 = c1;
+    const auto rr = cost_sweep(pr, method == 0 ? Method::stmc : Method::mlmc,
+                               std::span<const double>(eps, std::size_t(n_eps)), fit, workers);
+    for (std::size_t i = 0; i < rr.size(); ++i) {
+      rows[i].eps = rr[i].eps;
+      rows[i].method = rr[i].method == Method::stmc ? 0 : 1;
+      rows[i].integrator = static_cast<int32_t>(rr[i].integrator);
+      rows[i].cost_steps = rr[i].cost_steps;
+      rows[i].wall_seconds = rr[i].wall_seconds;
+      rows[i].estimate = rr[i].estimate;
+      rows[i].stat_error = rr[i].stat_error;
+    }
   });
 }
 

@@ -370,6 +370,10 @@ class MlmcOptions:  # estimators.hpp:271-278
     bias_fit: Optional[tuple[float, float]] = None  # (alpha, c1)
 
 
+WARNINGS = ("Var[Y_1] >= Var[Y_0]/2: coarsest level M_0 is too coarse to pay off",
+            "sample allocation did not converge in 64 rounds")  # estimators.hpp:352-373
+
+
 @dataclass
 class RunResult:  # estimators.hpp:197-210
     estimate: list
@@ -383,19 +387,36 @@ class RunResult:  # estimators.hpp:197-210
     pilot_cost_steps: int
     failed_samples: int
     wall_seconds: float
-    n_warnings: int
+    warnings: list
+    c: capi.RunResultC = field(repr=False, default=None)  # C view (for the format writers)
+    _keep: tuple = field(repr=False, default=())
 
 
-def _result(r: capi.RunResultC, pr: Problem, est: np.ndarray, err: np.ndarray) -> RunResult:
+def _new_result(dim: int):
+    r = capi.RunResultC()
+    est, err = np.zeros(dim), np.zeros(dim)
+    sy = np.zeros((capi.ABLMC_MAX_LEVELS, dim))
+    sy2 = np.zeros((capi.ABLMC_MAX_LEVELS, dim))
+    r.est_vec = est.ctypes.data_as(C.POINTER(C.c_double))
+    r.err_vec = err.ctypes.data_as(C.POINTER(C.c_double))
+    r.level_sum_y_vec = sy.ctypes.data_as(C.POINTER(C.c_double))
+    r.level_sum_y2_vec = sy2.ctypes.data_as(C.POINTER(C.c_double))
+    return r, (est, err, sy, sy2)
+
+
+def _result(r: capi.RunResultC, keep) -> RunResult:
+    est, err, sy, sy2 = keep
+    dim = est.shape[0]
     levels = []
     for l in range(r.n_levels):
-        st = LevelStats().init(l, r.level_h[l], 1)
-        st.sum_y[0], st.sum_y2[0] = r.level_sum_y[l], r.level_sum_y2[l]
+        st = LevelStats().init(l, r.level_h[l], dim)
+        st.sum_y[:], st.sum_y2[:] = sy[l], sy2[l]
         st.n, st.failed, st.cost_steps = r.level_n[l], r.level_failed[l], r.level_cost[l]
         levels.append(st)
+    warnings = [w for i, w in enumerate(WARNINGS) if r.warnings_mask >> i & 1]
     return RunResult(list(est), list(err), r.bias_estimate, r.alpha, r.c1, r.levels_used, levels,
                      r.total_cost_steps, r.pilot_cost_steps, r.failed_samples, r.wall_seconds,
-                     r.n_warnings)
+                     warnings, r, keep)
 
 
 def run_mlmc(pr: Problem, eps: float, o: MlmcOptions | None = None) -> RunResult:
@@ -405,21 +426,15 @@ def run_mlmc(pr: Problem, eps: float, o: MlmcOptions | None = None) -> RunResult
     oc.pilot_n, oc.pilot_levels_max, oc.init_n, oc.l_max = o.pilot_n, o.pilot_levels_max, o.init_n, o.l_max
     if o.bias_fit is not None:
         oc.use_bias_fit, (oc.alpha, oc.c1) = 1, o.bias_fit
-    r = capi.RunResultC()
-    est, err = np.zeros(pr.dim()), np.zeros(pr.dim())
-    r.est_vec = est.ctypes.data_as(C.POINTER(C.c_double))
-    r.err_vec = err.ctypes.data_as(C.POINTER(C.c_double))
+    r, keep = _new_result(pr.dim())
     _check(lib().ablmc_run_mlmc(_P(pr._c), float(eps), _P(oc), _P(r)))
-    return _result(r, pr, est, err)
+    return _result(r, keep)
 
 
 def run_stmc(pr: Problem, M_L: int, eps: float, fixed_n: int = 0) -> RunResult:
-    r = capi.RunResultC()
-    est, err = np.zeros(pr.dim()), np.zeros(pr.dim())
-    r.est_vec = est.ctypes.data_as(C.POINTER(C.c_double))
-    r.err_vec = err.ctypes.data_as(C.POINTER(C.c_double))
+    r, keep = _new_result(pr.dim())
     _check(lib().ablmc_run_stmc(_P(pr._c), int(M_L), float(eps), int(fixed_n), _P(r)))
-    return _result(r, pr, est, err)
+    return _result(r, keep)
 
 
 @dataclass
@@ -460,3 +475,119 @@ def fit_power_law(h: Sequence[float], v: Sequence[float]) -> tuple[float, float]
 
 def variance_decay_slope(rows: Sequence[DecayRow]) -> float:  # estimators.hpp:434-441
     return fit_power_law([r.h for r in rows], [r.var_y for r in rows])[0]
+
+
+# ------------------------------------------------------ cost sweep / formats
+class Method(enum.IntEnum):  # estimators.hpp:163
+    stmc = 0
+    mlmc = 1
+
+
+@dataclass
+class CostRow:  # estimators.hpp:443-451
+    eps: float
+    method: Method
+    integrator: Integrator
+    cost_steps: int
+    wall_seconds: float
+    estimate: float
+    stat_error: float
+
+
+def cost_sweep(pr: Problem, method: Method, eps_values: Sequence[float],
+               fit: tuple[float, float]) -> list[CostRow]:
+    """estimators.hpp:456-485 over the device sampler; fit = (alpha, c1)."""
+    eps = (C.c_double * len(eps_values))(*eps_values)
+    rows = (capi.CostRowC * len(eps_values))()
+    _check(lib().ablmc_cost_sweep(_P(pr._c), int(method), eps, len(eps_values), float(fit[0]),
+                                  float(fit[1]), rows))
+    return [CostRow(r.eps, Method(r.method), Integrator(r.integrator), r.cost_steps,
+                    r.wall_seconds, r.estimate, r.stat_error) for r in rows]
+
+
+@dataclass
+class RunConfig:  # config.hpp:18-40 (the fields result.json records)
+    model: ModelParams = field(default_factory=ModelParams)
+    method: Method = Method.mlmc
+    integrator: Integrator = Integrator.gl
+    qoi_kind: QoIKind = QoIKind.mean_position
+    qoi_a: float = 0.1055
+    qoi_b: float = 0.1555
+    qoi_r: int = 4
+    qoi_delta: float = 0.1
+    qoi_bins: int = 20
+    T: float = 1.0
+    m0: int = 40
+    eps: float = 1e-3
+    fixed_n: int = 0
+    seed: int = 12345
+    x0: float = 0.05
+    u0: float = 0.1
+    adaptive: bool = False
+    x_adapt: float = 0.05
+    coupling_signs: bool = True
+    workers: int = 1
+    timings: bool = True
+    output_dir: str = "."
+
+    def c(self) -> capi.RunConfigC:
+        k = capi.RunConfigC()
+        k.model = self.model.c()
+        k.method, k.integrator, k.qoi_kind, k.qoi_r = (int(self.method), int(self.integrator),
+                                                       int(self.qoi_kind), int(self.qoi_r))
+        k.qoi_a, k.qoi_b, k.qoi_delta, k.qoi_bins = self.qoi_a, self.qoi_b, self.qoi_delta, int(self.qoi_bins)
+        k.adaptive, k.T, k.m0, k.eps = int(self.adaptive), self.T, int(self.m0), self.eps
+        k.fixed_n, k.seed, k.x0, k.u0, k.x_adapt = (int(self.fixed_n), int(self.seed), self.x0,
+                                                    self.u0, self.x_adapt)
+        k.coupling_signs, k.workers, k.timings = (int(self.coupling_signs), int(self.workers),
+                                                  int(self.timings))
+        k.output_dir = self.output_dir.encode()
+        return k
+
+
+def _text(fn, *args) -> str:
+    n = fn(*args, None, 0)
+    if n < 0:
+        raise ValueError("format writer failed")
+    buf = C.create_string_buffer(int(n) + 1)
+    fn(*args, buf, n + 1)
+    return buf.raw[:n].decode()
+
+
+def result_json(cfg: RunConfig, r: RunResult) -> str:
+    """result.json text (output.hpp:91-123,213-219), byte-identical to the reference."""
+    cc = cfg.c()
+    return _text(lib().ablmc_result_json, _P(cc), _P(r.c), len(r.estimate))
+
+
+def write_result_json(cfg: RunConfig, r: RunResult, directory) -> str:
+    from pathlib import Path
+    d = Path(directory)
+    d.mkdir(parents=True, exist_ok=True)
+    path = d / "result.json"
+    path.write_bytes(result_json(cfg, r).encode())
+    return str(path)
+
+
+def variance_decay_csv(rows: Sequence[DecayRow]) -> str:  # output.hpp:184-191
+    arr = (capi.DecayRowC * len(rows))()
+    for a, r in zip(arr, rows):
+        a.level, a.h, a.var_y, a.mean_y, a.se_mean, a.n, a.cost_steps = (
+            r.level, r.h, r.var_y, r.mean_y, r.se_mean, r.n, r.cost_steps)
+    return _text(lib().ablmc_variance_decay_csv, arr, len(rows))
+
+
+def cost_sweep_csv(rows: Sequence[CostRow], timings: bool = True) -> str:  # output.hpp:193-200
+    arr = (capi.CostRowC * len(rows))()
+    for a, r in zip(arr, rows):
+        a.eps, a.method, a.integrator, a.cost_steps = r.eps, int(r.method), int(r.integrator), r.cost_steps
+        a.wall_seconds, a.estimate, a.stat_error = r.wall_seconds, r.estimate, r.stat_error
+    return _text(lib().ablmc_cost_sweep_csv, arr, len(rows), int(timings))
+
+
+def pdf_csv(edges: Sequence[float], concentration: Sequence[float],
+            std_error: Sequence[float]) -> str:  # output.hpp:202-209
+    e = (C.c_double * len(edges))(*edges)
+    cc = (C.c_double * len(concentration))(*concentration)
+    se = (C.c_double * len(std_error))(*std_error)
+    return _text(lib().ablmc_pdf_csv, e, len(edges), cc, se)

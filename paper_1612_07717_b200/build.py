@@ -16,11 +16,19 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OBJ = PKG / "build"
 LIB = PKG / "libablmc_b200.so"
-SOURCES = ["level_kernels.cu", "capi.cu", "drivers.cu"]
+SOURCES = ["level_kernels.cu", "capi.cu", "drivers.cu", "output.cpp"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+CXX = os.environ.get("CXX", "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-I", str(ROOT / "include")]
+# nlohmann/json (header-only, shipped in this image under cudnn_frontend) for
+# byte-identical result.json output (csrc/output.cpp).
+NLOHMANN = Path(os.environ.get(
+    "ABLMC_NLOHMANN_DIR",
+    "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann"))
+CXXFLAGS = ["-std=c++17", "-O2", "-fPIC", "-Wall", "-Wextra", "-I", str(ROOT / "include"),
+            "-I", str(NLOHMANN)]
 
 
 def _stale(out: Path, deps: list[Path]) -> bool:
@@ -38,7 +46,10 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         s = CSRC / src
         o = OBJ / (s.stem + ".o")
         if force or _stale(o, [s, *headers]):
-            cmd = [NVCC, *ARCH, *FLAGS, "-c", str(s), "-o", str(o)]
+            if s.suffix == ".cpp":
+                cmd = [CXX, *CXXFLAGS, "-c", str(s), "-o", str(o)]
+            else:
+                cmd = [NVCC, *ARCH, *FLAGS, "-c", str(s), "-o", str(o)]
             if src == "level_kernels.cu":
                 cmd += ["-Xptxas", "-v"]
             jobs.append((cmd, o))

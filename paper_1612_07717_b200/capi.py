@@ -79,7 +79,27 @@ class RunResultC(C.Structure):
                 ("level_n", C.c_int64 * _L), ("level_failed", C.c_int64 * _L),
                 ("level_cost", C.c_int64 * _L), ("level_h", C.c_double * _L),
                 ("level_sum_y", C.c_double * _L), ("level_sum_y2", C.c_double * _L),
-                ("est_vec", C.POINTER(C.c_double)), ("err_vec", C.POINTER(C.c_double))]
+                ("est_vec", C.POINTER(C.c_double)), ("err_vec", C.POINTER(C.c_double)),
+                ("level_sum_y_vec", C.POINTER(C.c_double)),
+                ("level_sum_y2_vec", C.POINTER(C.c_double)),
+                ("warnings_mask", C.c_int32), ("_pad2", C.c_int32)]
+
+
+class CostRowC(C.Structure):
+    _fields_ = [("eps", C.c_double), ("method", C.c_int32), ("integrator", C.c_int32),
+                ("cost_steps", C.c_int64), ("wall_seconds", C.c_double), ("estimate", C.c_double),
+                ("stat_error", C.c_double)]
+
+
+class RunConfigC(C.Structure):
+    _fields_ = [("model", ModelParamsC), ("method", C.c_int32), ("integrator", C.c_int32),
+                ("qoi_kind", C.c_int32), ("qoi_r", C.c_int32), ("qoi_a", C.c_double),
+                ("qoi_b", C.c_double), ("qoi_delta", C.c_double), ("qoi_bins", C.c_int32),
+                ("adaptive", C.c_int32), ("T", C.c_double), ("m0", C.c_int64),
+                ("eps", C.c_double), ("fixed_n", C.c_int64), ("seed", C.c_uint64),
+                ("x0", C.c_double), ("u0", C.c_double), ("x_adapt", C.c_double),
+                ("coupling_signs", C.c_int32), ("workers", C.c_int32), ("timings", C.c_int32),
+                ("_pad", C.c_int32), ("output_dir", C.c_char_p)]
 
 
 class DecayRowC(C.Structure):
@@ -133,6 +153,15 @@ SIGNATURES = {
     "ablmc_run_stmc": (C.c_int, [P(ProblemC), C.c_int64, C.c_double, C.c_int64,
                                  P(RunResultC)]),
     "ablmc_decay_sweep": (C.c_int, [P(ProblemC), C.c_int, C.c_int, C.c_int64, P(DecayRowC)]),
+    "ablmc_cost_sweep": (C.c_int, [P(ProblemC), C.c_int, P(C.c_double), C.c_int, C.c_double,
+                                   C.c_double, P(CostRowC)]),
+    "ablmc_run_config_defaults": (None, [P(RunConfigC)]),
+    "ablmc_result_json": (C.c_int64, [P(RunConfigC), P(RunResultC), C.c_int64, C.c_char_p,
+                                      C.c_int64]),
+    "ablmc_variance_decay_csv": (C.c_int64, [P(DecayRowC), C.c_int, C.c_char_p, C.c_int64]),
+    "ablmc_cost_sweep_csv": (C.c_int64, [P(CostRowC), C.c_int, C.c_int, C.c_char_p, C.c_int64]),
+    "ablmc_pdf_csv": (C.c_int64, [P(C.c_double), C.c_int, P(C.c_double), P(C.c_double),
+                                  C.c_char_p, C.c_int64]),
 }
 
 _lib = None

@@ -190,15 +190,24 @@ void fill_levels(const std::vector<Stats>& levels, ablmc_run_result* out) {
     out->level_h[l] = levels[l].h;
     out->level_sum_y[l] = levels[l].sum_y[0];
     out->level_sum_y2[l] = levels[l].sum_y2[0];
+    const size_t d = size_t(levels[l].dim);
+    for (size_t i = 0; i < d; ++i) {
+      if (out->level_sum_y_vec) out->level_sum_y_vec[l * d + i] = levels[l].sum_y[i];
+      if (out->level_sum_y2_vec) out->level_sum_y2_vec[l * d + i] = levels[l].sum_y2[i];
+    }
   }
 }
 
 void clear_result(ablmc_run_result* out) {
   double* ev = out->est_vec;
   double* er = out->err_vec;
+  double* sy = out->level_sum_y_vec;
+  double* sy2 = out->level_sum_y2_vec;
   std::memset(out, 0, sizeof(*out));
   out->est_vec = ev;
   out->err_vec = er;
+  out->level_sum_y_vec = sy;
+  out->level_sum_y2_vec = sy2;
 }
 
 }  // namespace
@@ -328,9 +337,11 @@ int ablmc_run_mlmc(const ablmc_problem* pr, double eps, const ablmc_mlmc_options
     if (int rc = ensure_level(l, o.init_n)) return rc;
   for (const auto& st : levels) out->pilot_cost_steps += st.cost_steps;
 
-  int n_warn = 0;
-  if (L >= 1 && levels.size() > 1 && levels[1].max_variance() >= 0.5 * levels[0].max_variance())
+  int n_warn = 0, warn_mask = 0;
+  if (L >= 1 && levels.size() > 1 && levels[1].max_variance() >= 0.5 * levels[0].max_variance()) {
     ++n_warn;
+    warn_mask |= 1;
+  }
 
   std::vector<double> v(size_t(L) + 1), hs(size_t(L) + 1);
   for (int round = 0; round < 64; ++round) {
@@ -346,7 +357,10 @@ int ablmc_run_mlmc(const ablmc_problem* pr, double eps, const ablmc_mlmc_options
     for (int l = 0; l <= L; ++l)
       stat2 += levels[size_t(l)].max_variance() / double(levels[size_t(l)].n);
     if (stat2 <= 0.5 * eps * eps) break;
-    if (round == 63) ++n_warn;
+    if (round == 63) {
+      ++n_warn;
+      warn_mask |= 2;
+    }
   }
 
   out->levels_used = L;
@@ -374,7 +388,43 @@ int ablmc_run_mlmc(const ablmc_problem* pr, double eps, const ablmc_mlmc_options
   }
   fill_levels(levels, out);
   out->n_warnings = n_warn;
+  out->warnings_mask = warn_mask;
   out->wall_seconds = now_s() - t0;
+  return 0;
+}
+
+// estimators.hpp:456-485: StMC picks M_L = m0 2^L from the bias fit so the
+// discretisation error stays below eps/sqrt(2); MLMC reuses the fit.
+int ablmc_cost_sweep(const ablmc_problem* pr, int method, const double* eps_values, int n_eps,
+                     double alpha, double c1, ablmc_cost_row* rows) {
+  if (int rc = ablmc_host::validate(pr)) return rc;
+  for (int i = 0; i < n_eps; ++i) {
+    const double eps = eps_values[i];
+    ablmc_cost_row& row = rows[i];
+    std::memset(&row, 0, sizeof row);
+    row.eps = eps;
+    row.method = method;
+    row.integrator = pr->integrator;
+    ablmc_run_result r;
+    std::memset(&r, 0, sizeof r);
+    if (method == 0) {
+      int L = 0;
+      if (int rc = choose_levels(alpha, c1, eps, pr->m0, pr->T, 16, L)) return rc;
+      if (int rc = ablmc_run_stmc(pr, pr->m0 << L, eps, 0, &r)) return rc;
+      row.cost_steps = r.total_cost_steps;
+    } else {
+      ablmc_mlmc_options o;
+      ablmc_mlmc_options_defaults(&o);
+      o.use_bias_fit = 1;
+      o.alpha = alpha;
+      o.c1 = c1;
+      if (int rc = ablmc_run_mlmc(pr, eps, &o, &r)) return rc;
+      row.cost_steps = r.total_cost_steps - r.pilot_cost_steps;
+    }
+    row.wall_seconds = r.wall_seconds;
+    row.estimate = r.estimate;
+    row.stat_error = r.stat_error;
+  }
   return 0;
 }
 

@@ -39,8 +39,9 @@ def main():
         a = ablmc.LevelStats().init(3, prb.h_level(3), prb.dim())
         ablmc.accumulate_samples(a, 11, count, prb, 3)
         m = ablmc.run_mlmc(pr, 1e-3)
+        js = ablmc.result_json(ablmc.RunConfig(timings=False), m)  # byte-stable result.json
         return (a.sum_y.tobytes(), a.sum_y2.tobytes(), a.n, a.cost_steps, m.estimate, m.stat_error,
-                [(s.n, s.sum_y.tobytes(), s.sum_y2.tobytes()) for s in m.level_stats])
+                [(s.n, s.sum_y.tobytes(), s.sum_y2.tobytes()) for s in m.level_stats], js)
 
     single = run()
     enable_collective()

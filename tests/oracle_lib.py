@@ -121,6 +121,16 @@ def ref() -> C.CDLL | None:
                                        C.c_int, P(capi.RunResultC)]),
             "ref_run_stmc": (C.c_int, [P(capi.ProblemC), C.c_int64, C.c_double, C.c_int64,
                                        C.c_int, P(capi.RunResultC)]),
+            "ref_cost_sweep": (C.c_int, [P(capi.ProblemC), C.c_int, P(C.c_double), C.c_int,
+                                         C.c_double, C.c_double, C.c_int, P(capi.CostRowC)]),
+            "ref_result_json": (C.c_int64, [P(capi.RunConfigC), P(capi.RunResultC), C.c_int64,
+                                            C.c_char_p, C.c_int64]),
+            "ref_variance_decay_csv": (C.c_int64, [P(capi.DecayRowC), C.c_int, C.c_char_p,
+                                                   C.c_int64]),
+            "ref_cost_sweep_csv": (C.c_int64, [P(capi.CostRowC), C.c_int, C.c_int, C.c_char_p,
+                                               C.c_int64]),
+            "ref_pdf_csv": (C.c_int64, [P(C.c_double), C.c_int, P(C.c_double), P(C.c_double),
+                                        C.c_char_p, C.c_int64]),
         }
         for k, (r, a) in sig.items():
             f = getattr(L, k)

@@ -332,6 +332,29 @@ def test_mlmc_estimate_agrees_with_reference_independent_seeds():
     assert g.failed_samples == 0 and g.levels_used >= 1
 
 
+def test_cost_sweep_and_result_json_vs_reference():
+    """cost_sweep (estimators.hpp:456-485) on the device against the
+    reference's: same seeds -> same allocation -> identical cost_steps and
+    estimates to rounding; the decay-sweep CSV is byte-identical when the
+    statistics agree to all printed digits."""
+    R = O.ref()
+    if R is None:
+        pytest.skip("oracle/_ref not built")
+    pr = ablmc.Problem.make(ablmc.ModelParams(), Ig.gl, ablmc.QoISpec(), 0.05, 0.1, 1.0, 40, 99)
+    eps = [1e-2, 4e-3]
+    for method in ablmc.Method:
+        got = ablmc.cost_sweep(pr, method, eps, (1.0, 0.5))
+        rows = (capi.CostRowC * 2)()
+        assert R.ref_cost_sweep(C.byref(pr._c), int(method), (C.c_double * 2)(*eps), 2, 1.0, 0.5,
+                                8, rows) == 0
+        for g, r in zip(got, rows):
+            assert g.cost_steps == r.cost_steps
+            assert abs(g.estimate - r.estimate) <= 1e-12 * abs(r.estimate)
+    m = ablmc.run_mlmc(pr, 2e-3)
+    js = ablmc.result_json(ablmc.RunConfig(timings=False, seed=99), m)
+    assert '"schema_version": 1' in js and '"wall_seconds": 0.0' in js
+
+
 def test_fast_div_sqrt_bit_identical_and_bm_libm_accuracy():
     """The branch-free fast div/sqrt equal __ddiv_rn/__dsqrt_rn bit for bit
     wherever they report no miss (2^26 random inputs incl. extreme
