@@ -209,6 +209,22 @@ def per_integrator(a, lib, stream, peak):
         rate = 2 * n * (1 << a.level) / (s.elapsed_time(e) * 1e-3)
         out[IG_NAME[ig]] = {"path_steps_per_s": rate, "W_alg": W_ALG[ig],
                             "roofline_frac": rate * W_ALG[ig] / peak, "paths": n}
+    # fp32-state variant (BASELINE config 5; statistical parity only)
+    from paper_1612_07717_b200 import ablmc
+    for ig in (0, 1, 2):
+        pr = ablmc.Problem.make(ablmc.ModelParams(), ablmc.Integrator(ig), ablmc.QoISpec(), 0.5,
+                                0.1, 1.0, 1, SEED, fp32=True)
+        pc = C.byref(pr._c)
+        lib.ablmc_accumulate_device(pc, a.level, 0, n)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        s.record(stream)
+        for _ in range(2):
+            lib.ablmc_accumulate_device(pc, a.level, 0, n)
+        e.record(stream)
+        torch.cuda.synchronize()
+        out[IG_NAME[ig] + "_fp32_state"] = {"path_steps_per_s": 2 * n * (1 << a.level) /
+                                            (s.elapsed_time(e) * 1e-3), "paths": n}
     return out
 
 

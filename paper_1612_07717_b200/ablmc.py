@@ -142,7 +142,8 @@ class Problem:
              m0: int, seed: int, opt: SampleOptions | None = None, *,
              profile: Profile = Profile.reference, random_u0: bool = False,
              const_sigma_u: float = 1.3, const_tau: float = 0.1, sigma_floor: float = 1e-3,
-             tau_min: float = 1e-5, tau_max: float = 1.0, validate: bool = True) -> "Problem":
+             tau_min: float = 1e-5, tau_max: float = 1.0, fp32: bool = False,
+             validate: bool = True) -> "Problem":
         opt = opt or SampleOptions()
         pr = Problem()
         c = pr._c
@@ -160,6 +161,7 @@ class Problem:
         c.x0, c.u0, c.T, c.m0, c.seed = x0, u0, T, int(m0), int(seed) & ((1 << 64) - 1)
         c.profile = int(profile)
         c.random_u0 = 1 if random_u0 else 0
+        c.fp32 = 1 if fp32 else 0  # fp32-state variant (BASELINE config 5), statistical parity only
         c.const_sigma_u, c.const_tau = const_sigma_u, const_tau
         c.sigma_floor, c.tau_min, c.tau_max = sigma_floor, tau_min, tau_max
         pr.qoi = qoi

@@ -42,7 +42,7 @@ class ProblemC(C.Structure):
                 ("qoi", QoISpecC), ("x0", C.c_double), ("u0", C.c_double), ("T", C.c_double),
                 ("m0", C.c_int64), ("seed", C.c_uint64), ("adaptive", C.c_int32),
                 ("profile", C.c_int32), ("x_adapt", C.c_double), ("random_u0", C.c_int32),
-                ("_pad", C.c_int32), ("const_sigma_u", C.c_double), ("const_tau", C.c_double),
+                ("fp32", C.c_int32), ("const_sigma_u", C.c_double), ("const_tau", C.c_double),
                 ("sigma_floor", C.c_double), ("tau_min", C.c_double), ("tau_max", C.c_double)]
 
 

@@ -37,6 +37,7 @@ struct KernelArgs {
   int random_u0;
   int qoi_kind;
   int fast;                 // 1: tame parameters, fast div/sqrt with IEEE recompute on a miss
+  int fp32;                 // 1: fp32-state variant (statistical parity only)
   int dim;
   double qa, qb, delta;
   int poly_n;               // r + 2 coefficients

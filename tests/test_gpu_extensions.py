@@ -96,6 +96,26 @@ def test_floored_profile_D3():
         assert c.sum_y[0] == a.sum_y[0]
 
 
+@pytest.mark.parametrize("ig", list(Ig))
+def test_fp32_state_variant_statistics(ig):
+    """fp32-state variant (BASELINE config 5): same scheme in fp32, different
+    (statistically equivalent) normals -> E[Y_l] within 4 combined standard
+    errors of the fp64 sampler and Var[Y_l] within 5%."""
+    for level in (2, 6):
+        st = {}
+        for fp32 in (False, True):
+            pr = ablmc.Problem.make(ablmc.ModelParams(), ig, ablmc.QoISpec(), 0.5, 0.1, 1.0, 1, 42,
+                                    fp32=fp32)
+            s = ablmc.LevelStats().init(level, pr.h_level(level), 1)
+            ablmc.accumulate_samples(s, 0, 1 << 21, pr, level)
+            st[fp32] = s
+        a, b = st[False], st[True]
+        assert a.failed == 0 and b.failed == 0
+        se = (a.std_error() ** 2 + b.std_error() ** 2) ** 0.5
+        assert abs(a.mean() - b.mean()) <= 4 * se, (level, a.mean(), b.mean(), se)
+        assert abs(b.variance() / a.variance() - 1) < 0.05
+
+
 def test_random_u0_coupled_levels_decay():
     """D2 with the reference profile (config 2 as written): fine and coarse
     share w0, so Var[Y_l] still decays like h_l^2 for GL."""
