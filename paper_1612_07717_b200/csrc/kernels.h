@@ -7,8 +7,10 @@
 
 #include "ablmc_device.cuh"
 
-#define ABLMC_TILE 256                 // samples per CTA tile
-#define ABLMC_TILES_PER_BLOCK 16       // 16 * 256 = 4096 = reference block_size (stats.hpp:100)
+#ifndef ABLMC_TILE
+#define ABLMC_TILE 256                 // samples per CTA tile (= threads per CTA)
+#endif
+#define ABLMC_TILES_PER_BLOCK (4096 / ABLMC_TILE)  // 4096 = reference block_size (stats.hpp:100)
 #define ABLMC_BLOCKS_PER_SUPER 1024    // 1024 * 4096 = 2^22 = ABLMC_SUPERBLOCK
 #define ABLMC_MAX_POLY 14
 #ifndef ABLMC_MINB_SE
@@ -18,7 +20,7 @@
 #define ABLMC_MINB_GL 3
 #endif
 #ifndef ABLMC_MINB_BAOAB
-#define ABLMC_MINB_BAOAB 2
+#define ABLMC_MINB_BAOAB 3
 #endif
 
 // Everything one launch needs, passed by value (kernel-parameter constant bank).
@@ -33,6 +35,7 @@ struct KernelArgs {
   int64_t offset;           // offset of this launch's sample 0 from `first`
   int64_t n;                // samples in this launch
   uint32_t k0, k1;          // Philox key of stream (seed, level)
+  ablmc_dev::PhiloxKey key; // its 10 round keys
   int signs_on;
   int random_u0;
   int qoi_kind;
