@@ -39,7 +39,8 @@ struct KernelArgs {
   int signs_on;
   int random_u0;
   int qoi_kind;
-  int fast;                 // 1: tame parameters, fast div/sqrt with IEEE recompute on a miss
+  int fast;                 // 1: tame parameters, fast div/sqrt with IEEE recompute on a miss;
+                            // 2: same with H == 1 and noise_scale == 1
   int fp32;                 // 1: fp32-state variant (statistical parity only)
   int dim;
   double qa, qb, delta;
