@@ -371,10 +371,15 @@ def run_b200(a):
     # per launch / its average launch duration (CUDA events on its stream)
     achieved = steps_per_launch * W_ALG[ig] / (k1_avg_ms * 1e-3)
     peak = fp64_rate.value
-    traffic = None  # DRAM bytes per K1 launch, scaled from the committed ncu capture
-    tp = ROOT / "profiles" / "k1_traffic.json"
+    # DRAM bytes per K1 launch and executed FP64-pipe instructions, scaled from
+    # the committed ncu capture of the same kernel (profiles/k1_ncu.json)
+    traffic, w_exec = None, None
+    tp = ROOT / "profiles" / "k1_ncu.json"
     if tp.exists():
-        traffic = json.loads(tp.read_text())["dram_bytes_per_path_step"] * steps_per_launch
+        prof = json.loads(tp.read_text()).get(IG_NAME[ig], {})
+        if "dram_bytes_per_path_step" in prof:
+            traffic = prof["dram_bytes_per_path_step"] * steps_per_launch
+            w_exec = prof["fp64_instr_per_path_step"]
 
     # ---- e2e: the public API call a user makes (accumulate_samples into a
     # host LevelStats) over the whole job's index range [0, world N); with
@@ -426,10 +431,16 @@ def run_b200(a):
                      "kernel": "k_level (K1, fused coupled level sampler)",
                      "kernel_avg_ms": k1_avg_ms, "kernel_share_of_step": k1_share,
                      "path_steps_per_launch": steps_per_launch,
+                     "W_alg": W_ALG[ig], "W_executed_ncu": w_exec,
+                     "frac_executed": (None if w_exec is None else
+                                       steps_per_launch * w_exec / (k1_avg_ms * 1e-3) / peak),
                      "note": f"achieved = coupled fine path-steps per K1 launch x W_alg="
-                             f"{W_ALG[ig]:.0f} FP64-pipe ops per path-step (SURVEY.md 8(d)) / K1 "
-                             "launch time; peak = DFMA probe measured in this run "
-                             "(MEASURED_PEAKS.json has no FP64 entry)"},
+                             f"{W_ALG[ig]:.0f} FP64-pipe ops per path-step (SURVEY.md 8(d)'s "
+                             "algorithmic count) / K1 launch time; frac_executed uses the FP64-pipe "
+                             "instructions ncu counts for this kernel (profiles/k1_ncu.json), i.e. "
+                             "the pipe utilisation; peak = DFMA probe measured in this run "
+                             "(MEASURED_PEAKS.json has no FP64 entry); traffic = ncu DRAM bytes "
+                             "per path-step x path-steps per launch"},
         "clocks": clk.summary(),
         "estimate": {"mean_y": acc.mean(), "n": acc.n, "failed": acc.failed},
     }
