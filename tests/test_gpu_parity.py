@@ -360,14 +360,15 @@ def test_fast_div_sqrt_bit_identical_and_bm_libm_accuracy():
     wherever they report no miss (2^26 random inputs incl. extreme
     exponents); the Box-Muller log/sincos kernels are within 1 ulp of
     libdevice (which is itself within 1-2 ulp of glibc)."""
-    out = (C.c_uint64 * 12)()
-    assert ablmc.lib().ablmc_selftest_fastmath(1 << 26, 12345, out) == 0
+    out = (C.c_uint64 * 15)()
+    assert ablmc.lib().ablmc_selftest_fastmath(1 << 28, 12345, out) == 0
     (div_n, div_bad, div_miss, sq_n, sq_bad, sq_miss, log_ulp, sin_e, cos_e, exp_ulp, em1_ulp,
-     em2_ulp) = list(out)
+     em2_ulp, dc_n, dc_bad, bm1_bad) = list(out)
+    assert dc_n == 1 << 28 and dc_bad == 0 and bm1_bad == 0
     print(f"div: {div_n} checked, {div_miss} misses; sqrt: {sq_n} checked, {sq_miss} misses; "
           f"log max ulp {log_ulp}; sin/cos max abs err {sin_e / 100}/{cos_e / 100} x 2^-53; "
           f"exp/expm1/expm1(2x) max ulp vs libdevice {exp_ulp}/{em1_ulp}/{em2_ulp}")
-    assert div_n == sq_n == 1 << 26
+    assert div_n == sq_n == 1 << 28
     assert div_bad == 0 and sq_bad == 0
     assert 0 < div_miss < div_n // 4 + div_n // 8 and 0 < sq_miss < sq_n // 4
     assert log_ulp <= 2 and sin_e <= 200 and cos_e <= 200
