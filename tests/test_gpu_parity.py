@@ -289,6 +289,41 @@ def test_edge_cases():
     assert close(acc.sum_y, ref.sum_y, 1e-11, 0)
     with pytest.raises(ValueError):
         ablmc.accumulate_samples(acc, 0, 10, pr, -1)
+    # negative first: the reference feeds uint64(idx) to the stream (wraps)
+    acc = ablmc.LevelStats().init(2, pr.h_level(2), 1)
+    ablmc.accumulate_samples(acc, -3000, 5000, pr, 2)
+    ref = O.Stats(1)
+    assert O.orc().orc_accumulate_samples(C.byref(pr._c), 2, -3000, 5000, C.byref(ref.c)) == 0
+    assert acc.n == ref.n and close(acc.sum_y, ref.sum_y, 1e-11, 1e-14)
+
+
+def test_long_paths_level16_vs_oracle():
+    """65536 fine + 32768 coarse steps per sample (M0 = 1, level 16)."""
+    for ig in Ig:
+        pr = ablmc.Problem.make(ablmc.ModelParams(), ig, ablmc.QoISpec(), 0.3, 0.1, 1.0, 1, 8)
+        got = ablmc.simulate_pairs(pr, 16, 0, 24)
+        p = O.default_params()
+        for i in range(0, 24, 5):
+            rc, f, c = O.orc_pair(int(ig), p, 0.3, 0.1, 1.0, 1 << 16, 8, 16, i)
+            assert rc == 0 and got["fok"][i] == 1
+            assert close([got["fx"][i], got["fu"][i], got["cx"][i], got["cu"][i]],
+                         [f.x, f.u, c.x, c.u], 1e-9, 1e-11), (ig, i)
+            assert (got["fn"][i], got["cn"][i]) == (f.n_refl, c.n_refl)
+
+
+def test_multi_chunk_call_equals_superblock_merge():
+    """A call spanning two launch chunks (chunk = 8 super-blocks for a scalar
+    QoI) gives the same bits as merging independently computed super-blocks."""
+    pr = ablmc.Problem.make(ablmc.ModelParams(), Ig.se, ablmc.QoISpec(), 0.5, 0.1, 1.0, 1, 4)
+    count = 9 * capi.ABLMC_SUPERBLOCK + 3
+    one = ablmc.LevelStats().init(1, pr.h_level(1), 1)
+    ablmc.accumulate_samples(one, 11, count, pr, 1)
+    parts = [ablmc.accumulate_partials(pr, 1, 11, count, lo, hi) for lo, hi in ((0, 4), (4, 10))]
+    acc = ablmc.LevelStats().init(1, pr.h_level(1), 1)
+    ablmc.merge_partials(acc, pr, 1, np.concatenate([p[0] for p in parts]),
+                         np.concatenate([p[1] for p in parts]))
+    assert acc.sum_y[0] == one.sum_y[0] and acc.sum_y2[0] == one.sum_y2[0]
+    assert (acc.n, acc.cost_steps) == (one.n, one.cost_steps) == (count, count * 3)
 
 
 # ------------------------------------------------------- statistics
