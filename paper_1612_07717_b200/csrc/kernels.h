@@ -47,6 +47,7 @@ struct KernelArgs {
   int poly_n;               // r + 2 coefficients
   double poly[ABLMC_MAX_POLY];
   const double* edges;      // device copy of bin edges (binned field)
+  double* pos;              // binned field: per-sample (x_f, x_c) of this launch (K1 -> K4)
 };
 
 struct StateOut {

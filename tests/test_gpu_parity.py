@@ -221,6 +221,31 @@ def test_binned_64_and_indicators_vs_oracle():
             assert close(acc.sum_y2, ref.sum_y2, 1e-11, 1e-11)
 
 
+@pytest.mark.parametrize("bins,delta,uneven", [(256, 0.1, True), (37, 1e-12, True),
+                                               (64, 0.3, False), (2, 0.05, False)])
+def test_binned_field_band_reduction_vs_oracle(bins, delta, uneven):
+    """K4 (banded binned field): many bins, non-equidistant edges, a delta so
+    small the band is disabled, a wide band, and a 2-bin field."""
+    rng = np.random.default_rng(bins)
+    if uneven:
+        inner = np.sort(rng.uniform(0.0, 1.0, bins - 1))
+        edges = [0.0] + inner.tolist() + [1.0]
+    else:
+        edges = ablmc.equidistant_edges(bins, 1.0)
+    q = ablmc.QoISpec(kind=ablmc.QoIKind.binned_field, bin_edges=edges, delta=delta)
+    for ig, level in ((Ig.gl, 0), (Ig.baoab, 3)):
+        pr = ablmc.Problem.make(ablmc.ModelParams(), ig, q, 0.02, 0.1, 1.0, 4, 13)
+        acc = ablmc.LevelStats().init(level, pr.h_level(level), bins)
+        ablmc.accumulate_samples(acc, 5, 3000, pr, level)
+        ref = O.Stats(bins)
+        assert O.orc().orc_accumulate_samples(C.byref(pr._c), level, 5, 3000, C.byref(ref.c)) == 0
+        assert (acc.n, acc.failed, acc.cost_steps) == (ref.n, ref.failed, ref.cost_steps)
+        assert close(acc.sum_y, ref.sum_y, 1e-11, 1e-11)
+        assert close(acc.sum_y2, ref.sum_y2, 1e-11, 1e-11)
+        if level == 0:  # components of each sample sum to exactly 1 (qoi.hpp:153-156)
+            assert abs(acc.sum_y.sum() - acc.n) <= 1e-9 * acc.n
+
+
 # ---------------------------------------------- determinism / partitioning
 def test_deterministic_and_add_merge():
     pr = ablmc.Problem.make(ablmc.ModelParams(), Ig.baoab, ablmc.QoISpec(), 0.05, 0.1, 1.0, 4, 9)
