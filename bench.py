@@ -314,9 +314,9 @@ def run_b200(a):
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
     res_s = torch.zeros(2, dtype=torch.float64, device="cuda")
-    res_c = torch.zeros(2, dtype=torch.int64, device="cuda")
+    res_c = torch.zeros(3, dtype=torch.int64, device="cuda")  # n, failed, cost_steps
     gat_s = torch.zeros(world, 2, dtype=torch.float64, device="cuda")
-    gat_c = torch.zeros(world, 2, dtype=torch.int64, device="cuda")
+    gat_c = torch.zeros(world, 3, dtype=torch.int64, device="cuda")
 
     def device_step():
         rc = lib.ablmc_accumulate_device(pc, level, first, N)

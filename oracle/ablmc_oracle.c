@@ -241,6 +241,153 @@ int orc_simulate_path(int ig, const ablmc_model_params* p, double x0, double u0,
   return rc;
 }
 
+/* ------------------------------------------------- adaptive (non-nested) */
+/* timeline.hpp:18-23 — min{h, lambda(x_adapt)/lambda(x) h} */
+static double adaptive_step_size(double x, double h, double x_adapt, const ablmc_model_params* p) {
+  const double lam_ref = orc_sde_coeffs(x_adapt, p).lambda;
+  const double lam_x = orc_sde_coeffs(x, p).lambda;
+  const double v = (lam_ref / lam_x) * h;
+  return (v < h) ? v : h; /* std::min(h, v) */
+}
+
+/* coupling.hpp:31-51 */
+int orc_simulate_path_adaptive(int ig, const ablmc_model_params* p, double x0, double u0,
+                               double T, double h_base, double x_adapt, uint64_t seed,
+                               uint32_t level, uint64_t idx, orc_state* out, int64_t* steps_out) {
+  orc_stream ns = {seed, level, idx, NULL, 0};
+  orc_state s = {x0, u0, +1, 0};
+  int64_t steps = 0;
+  const int64_t max_steps = 64 * (int64_t)ceil(T / h_base) + 64;
+  double t = 0.0;
+  int rc = 0;
+  while (t < T) {
+    double h = adaptive_step_size(s.x, h_base, x_adapt, p);
+    if (t + h >= T) h = T - t;
+    if (orc_step(ig, &s, h, stream_next(&ns), p, 0, NULL)) { rc = -1; break; }
+    t = (t + h >= T) ? T : t + h;
+    if (++steps > max_steps) { rc = -1; break; }
+  }
+  *out = s;
+  *steps_out = steps;
+  return rc;
+}
+
+/* timeline.hpp:75-105: the adaptive increments over the pending sub-intervals */
+static double increment_se(const double* xi, const double* dt, const int* sg, int n, int sc,
+                           int is_coarse) {
+  double acc = 0.0;
+  for (int j = 0; j < n; ++j) {
+    const double s = is_coarse ? (double)sg[j] : 1.0;
+    acc += s * xi[j] * sqrt(dt[j]);
+  }
+  return (is_coarse ? sc : 1) * acc;
+}
+static double increment_gl(const double* xi, const double* dt, const double* lam, const int* sg,
+                           int n, int sc, int is_coarse) {
+  double acc = 0.0, damp = 1.0;
+  for (int r = n; r-- > 0;) {
+    const double s = is_coarse ? (double)sg[r] : 1.0;
+    acc += s * xi[r] * ou_noise_sd(lam[r], dt[r]) * damp;
+    damp *= exp(-lam[r] * dt[r]);
+  }
+  return (is_coarse ? sc : 1) * acc;
+}
+
+#define ORC_MAX_PENDING 65536
+typedef struct {
+  orc_state s;
+  double t, h_cur, t_next;
+  int done;
+  int64_t steps;
+  int n;
+  double xi[ORC_MAX_PENDING], dt[ORC_MAX_PENDING], lam[ORC_MAX_PENDING];
+  int sg[ORC_MAX_PENDING];
+} orc_leg;
+
+static void leg_schedule(orc_leg* L, double base, double T, double x_adapt,
+                         const ablmc_model_params* p) {
+  double h = adaptive_step_size(L->s.x, base, x_adapt, p);
+  if (L->t + h >= T) {
+    h = T - L->t;
+    L->t_next = T;
+  } else {
+    L->t_next = L->t + h;
+  }
+  L->h_cur = h;
+}
+
+static int leg_take(int ig, orc_leg* L, int is_coarse, const ablmc_model_params* p) {
+  double xi_eq;
+  if (ig == ABLMC_SE) {
+    const double dw = increment_se(L->xi, L->dt, L->sg, L->n, is_coarse ? L->s.parity : 1, is_coarse);
+    xi_eq = dw / sqrt(L->h_cur);
+  } else {
+    const double g = increment_gl(L->xi, L->dt, L->lam, L->sg, L->n, is_coarse ? L->s.parity : 1,
+                                  is_coarse);
+    xi_eq = g / ou_noise_sd(L->lam[0], L->h_cur);
+  }
+  if (orc_step(ig, &L->s, L->h_cur, xi_eq, p, 0, NULL)) return -1;
+  L->t = L->t_next;
+  ++L->steps;
+  L->n = 0;
+  return 0;
+}
+
+/* coupling.hpp:137-214 */
+int orc_simulate_pair_adaptive(int ig, const ablmc_model_params* p, double x0, double u0,
+                               double T, double h_base, double x_adapt, uint64_t seed,
+                               uint32_t level, uint64_t idx, int signs_on, orc_state* fine,
+                               orc_state* coarse, int64_t* steps_out) {
+  orc_stream ns = {seed, level, idx, NULL, 0};
+  static __thread orc_leg F, Cc;
+  orc_leg* f = &F;
+  orc_leg* c = &Cc;
+  f->s = (orc_state){x0, u0, +1, 0};
+  f->t = 0.0; f->done = 0; f->steps = 0; f->n = 0;
+  *c = *f;
+  leg_schedule(f, h_base, T, x_adapt, p);
+  leg_schedule(c, 2.0 * h_base, T, x_adapt, p);
+  const int64_t max_iter = 256 * (int64_t)ceil(T / h_base) + 256;
+  int64_t iter = 0;
+  double t = 0.0;
+  int rc = 0;
+  while (!f->done || !c->done) {
+    const double a = f->done ? T : f->t_next, b = c->done ? T : c->t_next;
+    const double tau_next = (b < a) ? b : a; /* std::min */
+    const double dt = tau_next - t;
+    if (dt > 0.0) {
+      const double xi = stream_next(&ns);
+      const int sf = signs_on ? f->s.parity : 1;
+      if (!f->done) {
+        if (f->n >= ORC_MAX_PENDING) { rc = -2; break; }
+        f->xi[f->n] = xi; f->dt[f->n] = dt; f->lam[f->n] = orc_sde_coeffs(f->s.x, p).lambda;
+        f->sg[f->n++] = 1;
+      }
+      if (!c->done) {
+        if (c->n >= ORC_MAX_PENDING) { rc = -2; break; }
+        c->xi[c->n] = xi; c->dt[c->n] = dt; c->lam[c->n] = orc_sde_coeffs(c->s.x, p).lambda;
+        c->sg[c->n++] = sf;
+      }
+    }
+    if (!f->done && f->t_next == tau_next) {
+      if (leg_take(ig, f, 0, p)) { rc = -1; break; }
+      if (f->t_next >= T) f->done = 1;
+      else leg_schedule(f, h_base, T, x_adapt, p);
+    }
+    if (!c->done && c->t_next == tau_next) {
+      if (leg_take(ig, c, 1, p)) { rc = -1; break; }
+      if (c->t_next >= T) c->done = 1;
+      else leg_schedule(c, 2.0 * h_base, T, x_adapt, p);
+    }
+    t = tau_next;
+    if (++iter > max_iter) { rc = -1; break; }
+  }
+  *fine = f->s;
+  *coarse = c->s;
+  *steps_out = f->steps + c->steps;
+  return rc;
+}
+
 /* qoi.hpp:31-77 — Gaussian elimination with partial pivoting. */
 int orc_build_smoothing_polynomial(int r, double* x) {
   if (r < 0 || r > 12) return -1;
@@ -329,21 +476,34 @@ static int64_t one_sample(const ablmc_problem* pr, const double* poly, int coupl
   const ablmc_model_params* p = &pr->params;
   if (coupled) {
     orc_state f, c;
-    if (orc_simulate_pair(pr->integrator, p, pr->x0, pr->u0, pr->T, M, pr->seed,
-                          (uint32_t)level, (uint64_t)idx, NULL, pr->signs_on, &f, &c))
-      return -1;
+    int64_t steps = M + M / 2;
+    int rc;
+    if (pr->adaptive) /* coupling.hpp:262-265 */
+      rc = orc_simulate_pair_adaptive(pr->integrator, p, pr->x0, pr->u0, pr->T, pr->T / (double)M,
+                                      pr->x_adapt, pr->seed, (uint32_t)level, (uint64_t)idx,
+                                      pr->signs_on, &f, &c, &steps);
+    else
+      rc = orc_simulate_pair(pr->integrator, p, pr->x0, pr->u0, pr->T, M, pr->seed,
+                             (uint32_t)level, (uint64_t)idx, NULL, pr->signs_on, &f, &c);
+    if (rc) return -1;
     orc_evaluate(&pr->qoi, poly, pr->qoi.r, f.x, y);
     orc_evaluate(&pr->qoi, poly, pr->qoi.r, c.x, scratch);
     const int64_t d = qoi_dim(&pr->qoi);
     for (int64_t i = 0; i < d; ++i) y[i] -= scratch[i];
-    return M + M / 2;
+    return steps;
   }
   orc_state s;
-  if (orc_simulate_path(pr->integrator, p, pr->x0, pr->u0, pr->T, M, pr->seed, stream_level,
-                        (uint64_t)idx, NULL, &s))
-    return -1;
+  int64_t steps = M;
+  int rc;
+  if (pr->adaptive) /* coupling.hpp:238-240 */
+    rc = orc_simulate_path_adaptive(pr->integrator, p, pr->x0, pr->u0, pr->T, pr->T / (double)M,
+                                    pr->x_adapt, pr->seed, stream_level, (uint64_t)idx, &s, &steps);
+  else
+    rc = orc_simulate_path(pr->integrator, p, pr->x0, pr->u0, pr->T, M, pr->seed, stream_level,
+                           (uint64_t)idx, NULL, &s);
+  if (rc) return -1;
   orc_evaluate(&pr->qoi, poly, pr->qoi.r, s.x, y);
-  return M;
+  return steps;
 }
 
 /* stats.hpp:96-136 (the result is independent of the worker count, so one

@@ -201,7 +201,11 @@ void ref_pair_states(const ablmc_problem* pr, int level, int64_t first, int64_t 
     NoiseStream ns(pr->seed, uint32_t(level), uint64_t(first + i));
     try {
       const PairResult r =
-          simulate_pair(to_ig(pr->integrator), p, pr->x0, pr->u0, pr->T, M, ns, pr->signs_on != 0);
+          pr->adaptive
+              ? simulate_pair_adaptive(to_ig(pr->integrator), p, pr->x0, pr->u0, pr->T,
+                                       pr->T / double(M), pr->x_adapt, ns, pr->signs_on != 0)
+              : simulate_pair(to_ig(pr->integrator), p, pr->x0, pr->u0, pr->T, M, ns,
+                              pr->signs_on != 0);
       put_state(r.fine, &out[i].fine, 1);
       put_state(r.coarse, &out[i].coarse, 1);
     } catch (const UnstableStepError&) {
@@ -216,7 +220,10 @@ void ref_path_states(const ablmc_problem* pr, int64_t M, uint32_t stream_level, 
   for (int64_t i = 0; i < count; ++i) {
     NoiseStream ns(pr->seed, stream_level, uint64_t(first + i));
     try {
-      const PathResult r = simulate_path(to_ig(pr->integrator), p, pr->x0, pr->u0, pr->T, M, ns);
+      const PathResult r =
+          pr->adaptive ? simulate_path_adaptive(to_ig(pr->integrator), p, pr->x0, pr->u0, pr->T,
+                                                pr->T / double(M), pr->x_adapt, ns)
+                       : simulate_path(to_ig(pr->integrator), p, pr->x0, pr->u0, pr->T, M, ns);
       put_state(r.state, &out[i], 1);
     } catch (const UnstableStepError&) {
       out[i].ok = 0;

@@ -299,7 +299,7 @@ def accumulate_partials(pr: Problem, level: int, first: int, count: int, sb_begi
     n = sb_end - sb_begin
     dim = pr.dim()
     sums = np.zeros((max(n, 0), 2 * dim))
-    counts = np.zeros((max(n, 0), 2), dtype=np.int64)
+    counts = np.zeros((max(n, 0), capi.ABLMC_NCOUNTS), dtype=np.int64)  # n, failed, cost_steps
     _check(lib().ablmc_accumulate_partials(
         _P(pr._c), int(level), int(M), int(stream_level), int(first), int(count), int(sb_begin),
         int(sb_end), sums.ctypes.data_as(C.POINTER(C.c_double)),

@@ -19,6 +19,7 @@ ABLMC_ERR_SAMPLE_FAILURE = 3
 ABLMC_ERR_CUDA = 4
 ABLMC_ERR_NO_DEVICE = 5
 ABLMC_SUPERBLOCK = 1 << 22
+ABLMC_NCOUNTS = 3  # {n, failed, cost_steps} per super-block partial
 ABLMC_MAX_LEVELS = 24
 
 SE, GL, BAOAB = 0, 1, 2

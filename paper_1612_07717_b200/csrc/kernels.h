@@ -13,6 +13,8 @@
 #define ABLMC_TILES_PER_BLOCK (4096 / ABLMC_TILE)  // 4096 = reference block_size (stats.hpp:100)
 #define ABLMC_BLOCKS_PER_SUPER 1024    // 1024 * 4096 = 2^22 = ABLMC_SUPERBLOCK
 #define ABLMC_MAX_POLY 14
+// per tile / block / super-block count record: {n, failed, cost_steps}
+constexpr int kCnt = 3;
 #ifndef ABLMC_MINB_SE
 #define ABLMC_MINB_SE 4
 #endif
@@ -58,10 +60,10 @@ struct StateOut {
 };
 
 cudaError_t launch_level(const KernelArgs& a, int ig, bool coupled, double* tile_sums,
-                         int* tile_cnt, cudaStream_t st);
+                         long long* tile_cnt, cudaStream_t st);
 cudaError_t launch_states(const KernelArgs& a, int ig, bool coupled, const double* xi,
                           StateOut* out, cudaStream_t st);
-cudaError_t launch_merge_tiles(int64_t n_tiles, int dim, const double* ts, const int* tc,
+cudaError_t launch_merge_tiles(int64_t n_tiles, int dim, const double* ts, const long long* tc,
                                double* bs, long long* bc, cudaStream_t st);
 cudaError_t launch_merge_blocks(int64_t n_blk, int dim, const double* bs, const long long* bc,
                                 double* ss, long long* sc, int64_t sb_base, cudaStream_t st);

@@ -87,9 +87,9 @@ def accumulate_sharded(acc: ablmc.LevelStats, first: int, count: int, pr: ablmc.
     if hi > lo:
         sums, cnts = fn(pr, level, first, count, lo, hi)
     else:
-        sums, cnts = np.zeros((0, 2 * dim)), np.zeros((0, 2), dtype=np.int64)
+        sums, cnts = np.zeros((0, 2 * dim)), np.zeros((0, capi.ABLMC_NCOUNTS), dtype=np.int64)
     # pack (sums | counts as exact float64 bit patterns) into one buffer per rank
-    width = 2 * dim + 2
+    width = 2 * dim + capi.ABLMC_NCOUNTS
     cap = (n_sb + world - 1) // world
     buf = np.zeros((cap, width))
     buf[: hi - lo, : 2 * dim] = sums

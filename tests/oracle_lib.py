@@ -66,6 +66,15 @@ def orc() -> C.CDLL:
             "orc_simulate_path": (C.c_int, [C.c_int, P(capi.ModelParamsC), C.c_double, C.c_double,
                                             C.c_double, C.c_int64, C.c_uint64, C.c_uint32,
                                             C.c_uint64, P(C.c_double), P(OrcState)]),
+            "orc_simulate_pair_adaptive": (C.c_int, [C.c_int, P(capi.ModelParamsC), C.c_double,
+                                                     C.c_double, C.c_double, C.c_double,
+                                                     C.c_double, C.c_uint64, C.c_uint32,
+                                                     C.c_uint64, C.c_int, P(OrcState),
+                                                     P(OrcState), P(C.c_int64)]),
+            "orc_simulate_path_adaptive": (C.c_int, [C.c_int, P(capi.ModelParamsC), C.c_double,
+                                                     C.c_double, C.c_double, C.c_double,
+                                                     C.c_double, C.c_uint64, C.c_uint32,
+                                                     C.c_uint64, P(OrcState), P(C.c_int64)]),
             "orc_build_smoothing_polynomial": (C.c_int, [C.c_int, P(C.c_double)]),
             "orc_evaluate": (None, [P(capi.QoISpecC), P(C.c_double), C.c_int, C.c_double,
                                     P(C.c_double)]),
@@ -202,3 +211,18 @@ def orc_path(ig, params, x0, u0, T, M, seed, level, idx, xi=None):
     rc = orc().orc_simulate_path(ig, C.byref(params), x0, u0, T, M, seed, level, idx, xp,
                                  C.byref(s))
     return rc, s
+
+
+def orc_pair_adaptive(ig, params, x0, u0, T, h_base, x_adapt, seed, level, idx, signs_on=1):
+    f, c, n = OrcState(), OrcState(), C.c_int64(0)
+    rc = orc().orc_simulate_pair_adaptive(ig, C.byref(params), x0, u0, T, h_base, x_adapt, seed,
+                                          level, idx, signs_on, C.byref(f), C.byref(c),
+                                          C.byref(n))
+    return rc, f, c, n.value
+
+
+def orc_path_adaptive(ig, params, x0, u0, T, h_base, x_adapt, seed, level, idx):
+    s, n = OrcState(), C.c_int64(0)
+    rc = orc().orc_simulate_path_adaptive(ig, C.byref(params), x0, u0, T, h_base, x_adapt, seed,
+                                          level, idx, C.byref(s), C.byref(n))
+    return rc, s, n.value

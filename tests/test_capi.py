@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version():
-    assert capi.load().ablmc_abi_version() == 1
+    assert capi.load().ablmc_abi_version() == 2
 
 
 def test_struct_layouts_match_header(tmp_path):
@@ -161,7 +161,7 @@ def test_count_zero_is_a_noop_without_touching_the_device():
 def test_merge_partials_is_ordered_add_merge():
     pr = mk()
     sums = np.array([[1.0, 1.0], [2.0, 4.0], [0.5, 0.25]])
-    counts = np.array([[3, 0], [4, 1], [2, 0]], dtype=np.int64)
+    counts = np.array([[3, 0, 3 * 120], [4, 1, 4 * 120], [2, 0, 2 * 120]], dtype=np.int64)
     acc = ablmc.LevelStats().init(1, 0.0125, 1)
     acc.sum_y[0] = 10.0
     ablmc.merge_partials(acc, pr, 1, sums, counts)

@@ -174,8 +174,14 @@ def test_pairs_bit_exact(ref_vectors):
         p = _params(d)
         M = d["m0"] << case["level"]
         for i, st in enumerate(case["states"]):
-            rc, f, c = O.orc_pair(d["integrator"], p, d["x0"], d["u0"], d["T"], M, d["seed"],
-                                  case["level"], case["first"] + i, signs_on=d["signs_on"])
+            if d.get("adaptive"):
+                rc, f, c, _ = O.orc_pair_adaptive(d["integrator"], p, d["x0"], d["u0"], d["T"],
+                                                  d["T"] / M, d["x_adapt"], d["seed"],
+                                                  case["level"], case["first"] + i,
+                                                  signs_on=d["signs_on"])
+            else:
+                rc, f, c = O.orc_pair(d["integrator"], p, d["x0"], d["u0"], d["T"], M, d["seed"],
+                                      case["level"], case["first"] + i, signs_on=d["signs_on"])
             assert (rc == 0) == bool(st[4]), case["name"]
             if rc == 0:
                 got = [f.x.hex(), f.u.hex(), f.parity, f.n_refl, 1, c.x.hex(), c.u.hex(), c.parity,
@@ -188,8 +194,13 @@ def test_paths_bit_exact(ref_vectors):
         d = case["problem"]
         p = _params(d)
         for i, st in enumerate(case["states"]):
-            rc, s = O.orc_path(d["integrator"], p, d["x0"], d["u0"], d["T"], case["M"], d["seed"],
-                               case["stream_level"], case["first"] + i)
+            if d.get("adaptive"):
+                rc, s, _ = O.orc_path_adaptive(d["integrator"], p, d["x0"], d["u0"], d["T"],
+                                               d["T"] / case["M"], d["x_adapt"], d["seed"],
+                                               case["stream_level"], case["first"] + i)
+            else:
+                rc, s = O.orc_path(d["integrator"], p, d["x0"], d["u0"], d["T"], case["M"],
+                                   d["seed"], case["stream_level"], case["first"] + i)
             assert rc == 0 and [s.x.hex(), s.u.hex(), s.parity, s.n_refl, 1] == st
 
 
@@ -204,6 +215,7 @@ def problem_from(d):
         pr.qoi.n_edges = len(d["edges"])
         pr.qoi.bin_edges = C.cast(keep, P(C.c_double))
     pr.x0, pr.u0, pr.T, pr.m0, pr.seed = d["x0"], d["u0"], d["T"], d["m0"], d["seed"]
+    pr.adaptive, pr.x_adapt = d.get("adaptive", 0), d.get("x_adapt", 0.05)
     return pr, keep
 
 

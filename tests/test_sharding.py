@@ -22,14 +22,14 @@ SB = 1000  # small super-blocks so a CPU-sized count spans several of them
 def oracle_partials(pr, level, first, count, lo, hi):
     dim = pr.dim()
     sums = np.zeros((hi - lo, 2 * dim))
-    cnts = np.zeros((hi - lo, 2), dtype=np.int64)
+    cnts = np.zeros((hi - lo, 3), dtype=np.int64)
     for i, sb in enumerate(range(lo, hi)):
         a = sb * SB
         n = min(SB, count - a)
         st = O.Stats(dim)
         assert O.orc().orc_accumulate_samples(C.byref(pr._c), level, first + a, n, C.byref(st.c)) == 0
         sums[i, :dim], sums[i, dim:] = st.sum_y, st.sum_y2
-        cnts[i] = (st.n, st.failed)
+        cnts[i] = (st.n, st.failed, st.cost_steps)
     return sums, cnts
 
 
