@@ -253,8 +253,9 @@ static double adaptive_step_size(double x, double h, double x_adapt, const ablmc
 /* coupling.hpp:31-51 */
 int orc_simulate_path_adaptive(int ig, const ablmc_model_params* p, double x0, double u0,
                                double T, double h_base, double x_adapt, uint64_t seed,
-                               uint32_t level, uint64_t idx, orc_state* out, int64_t* steps_out) {
-  orc_stream ns = {seed, level, idx, NULL, 0};
+                               uint32_t level, uint64_t idx, const double* xi, orc_state* out,
+                               int64_t* steps_out) {
+  orc_stream ns = {seed, level, idx, xi, 0};
   orc_state s = {x0, u0, +1, 0};
   int64_t steps = 0;
   const int64_t max_steps = 64 * (int64_t)ceil(T / h_base) + 64;
@@ -336,9 +337,9 @@ static int leg_take(int ig, orc_leg* L, int is_coarse, const ablmc_model_params*
 /* coupling.hpp:137-214 */
 int orc_simulate_pair_adaptive(int ig, const ablmc_model_params* p, double x0, double u0,
                                double T, double h_base, double x_adapt, uint64_t seed,
-                               uint32_t level, uint64_t idx, int signs_on, orc_state* fine,
-                               orc_state* coarse, int64_t* steps_out) {
-  orc_stream ns = {seed, level, idx, NULL, 0};
+                               uint32_t level, uint64_t idx, const double* xi_in, int signs_on,
+                               orc_state* fine, orc_state* coarse, int64_t* steps_out) {
+  orc_stream ns = {seed, level, idx, xi_in, 0};
   static __thread orc_leg F, Cc;
   orc_leg* f = &F;
   orc_leg* c = &Cc;
@@ -481,7 +482,7 @@ static int64_t one_sample(const ablmc_problem* pr, const double* poly, int coupl
     if (pr->adaptive) /* coupling.hpp:262-265 */
       rc = orc_simulate_pair_adaptive(pr->integrator, p, pr->x0, pr->u0, pr->T, pr->T / (double)M,
                                       pr->x_adapt, pr->seed, (uint32_t)level, (uint64_t)idx,
-                                      pr->signs_on, &f, &c, &steps);
+                                      NULL, pr->signs_on, &f, &c, &steps);
     else
       rc = orc_simulate_pair(pr->integrator, p, pr->x0, pr->u0, pr->T, M, pr->seed,
                              (uint32_t)level, (uint64_t)idx, NULL, pr->signs_on, &f, &c);
@@ -497,7 +498,8 @@ static int64_t one_sample(const ablmc_problem* pr, const double* poly, int coupl
   int rc;
   if (pr->adaptive) /* coupling.hpp:238-240 */
     rc = orc_simulate_path_adaptive(pr->integrator, p, pr->x0, pr->u0, pr->T, pr->T / (double)M,
-                                    pr->x_adapt, pr->seed, stream_level, (uint64_t)idx, &s, &steps);
+                                    pr->x_adapt, pr->seed, stream_level, (uint64_t)idx, NULL, &s,
+                                    &steps);
   else
     rc = orc_simulate_path(pr->integrator, p, pr->x0, pr->u0, pr->T, M, pr->seed, stream_level,
                            (uint64_t)idx, NULL, &s);

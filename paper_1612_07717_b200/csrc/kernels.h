@@ -50,13 +50,18 @@ struct KernelArgs {
   double poly[ABLMC_MAX_POLY];
   const double* edges;      // device copy of bin edges (binned field)
   double* pos;              // binned field: per-sample (x_f, x_c) of this launch (K1 -> K4)
+  // adaptive (non-nested) stepping, coupling.hpp:31-51 / 137-214
+  int adaptive;
+  double T, x_adapt;
+  double h_base;            // T / M: fine base step (coarse base 2 h_base)
+  int64_t max_iter;         // pair: 256 ceil(T/h_base) + 256; path: 64 ceil(T/h_base) + 64
 };
 
 struct StateOut {
   double fx, fu, cx, cu;
   int fpar, cpar;
   int fn, cn;
-  int ok, pad;
+  int ok, steps;             // steps: adaptive steps taken (fine + coarse)
 };
 
 cudaError_t launch_level(const KernelArgs& a, int ig, bool coupled, double* tile_sums,

@@ -69,12 +69,13 @@ def orc() -> C.CDLL:
             "orc_simulate_pair_adaptive": (C.c_int, [C.c_int, P(capi.ModelParamsC), C.c_double,
                                                      C.c_double, C.c_double, C.c_double,
                                                      C.c_double, C.c_uint64, C.c_uint32,
-                                                     C.c_uint64, C.c_int, P(OrcState),
-                                                     P(OrcState), P(C.c_int64)]),
+                                                     C.c_uint64, P(C.c_double), C.c_int,
+                                                     P(OrcState), P(OrcState), P(C.c_int64)]),
             "orc_simulate_path_adaptive": (C.c_int, [C.c_int, P(capi.ModelParamsC), C.c_double,
                                                      C.c_double, C.c_double, C.c_double,
                                                      C.c_double, C.c_uint64, C.c_uint32,
-                                                     C.c_uint64, P(OrcState), P(C.c_int64)]),
+                                                     C.c_uint64, P(C.c_double), P(OrcState),
+                                                     P(C.c_int64)]),
             "orc_build_smoothing_polynomial": (C.c_int, [C.c_int, P(C.c_double)]),
             "orc_evaluate": (None, [P(capi.QoISpecC), P(C.c_double), C.c_int, C.c_double,
                                     P(C.c_double)]),
@@ -213,16 +214,28 @@ def orc_path(ig, params, x0, u0, T, M, seed, level, idx, xi=None):
     return rc, s
 
 
-def orc_pair_adaptive(ig, params, x0, u0, T, h_base, x_adapt, seed, level, idx, signs_on=1):
+def _xi_ptr(xi):
+    if xi is None:
+        return None, None
+    xi = np.ascontiguousarray(xi, dtype=np.float64)
+    return xi, xi.ctypes.data_as(P(C.c_double))
+
+
+def orc_pair_adaptive(ig, params, x0, u0, T, h_base, x_adapt, seed, level, idx, signs_on=1,
+                      xi=None):
+    """xi: explicit NoiseStream::next() sequence (long enough for the pair's
+    data-dependent draw count), else the Philox stream."""
     f, c, n = OrcState(), OrcState(), C.c_int64(0)
+    keep, xp = _xi_ptr(xi)
     rc = orc().orc_simulate_pair_adaptive(ig, C.byref(params), x0, u0, T, h_base, x_adapt, seed,
-                                          level, idx, signs_on, C.byref(f), C.byref(c),
+                                          level, idx, xp, signs_on, C.byref(f), C.byref(c),
                                           C.byref(n))
     return rc, f, c, n.value
 
 
-def orc_path_adaptive(ig, params, x0, u0, T, h_base, x_adapt, seed, level, idx):
+def orc_path_adaptive(ig, params, x0, u0, T, h_base, x_adapt, seed, level, idx, xi=None):
     s, n = OrcState(), C.c_int64(0)
+    keep, xp = _xi_ptr(xi)
     rc = orc().orc_simulate_path_adaptive(ig, C.byref(params), x0, u0, T, h_base, x_adapt, seed,
-                                          level, idx, C.byref(s), C.byref(n))
+                                          level, idx, xp, C.byref(s), C.byref(n))
     return rc, s, n.value

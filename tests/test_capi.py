@@ -104,7 +104,12 @@ def test_validation_errors_mirror_reference():
     with pytest.raises(ValueError, match="r must be"):
         mk(qoi=ablmc.QoISpec(r=13))
     with pytest.raises(ValueError, match="adaptive"):
-        mk(opt=ablmc.SampleOptions(adaptive=True))
+        mk(opt=ablmc.SampleOptions(adaptive=True), random_u0=True)
+    with pytest.raises(ValueError, match="adaptive"):
+        mk(opt=ablmc.SampleOptions(adaptive=True), fp32=True)
+    with pytest.raises(ValueError, match="x_adapt"):
+        mk(opt=ablmc.SampleOptions(adaptive=True, x_adapt=0.0))
+    mk(opt=ablmc.SampleOptions(adaptive=True))  # coupling.hpp:137-214 on the device
     mk()  # defaults validate
 
 
