@@ -55,6 +55,12 @@ struct KernelArgs {
   double T, x_adapt;
   double h_base;            // T / M: fine base step (coarse base 2 h_base)
   int64_t max_iter;         // pair: 256 ceil(T/h_base) + 256; path: 64 ceil(T/h_base) + 64
+  // persistent adaptive sampler (K1P -> K1R -> K1T): per-sample results of
+  // this launch, work counters {next sample, redo count}, redo list
+  double* ad_y;             // QoI value (scalar kinds)
+  long long* ad_steps;      // steps taken, -1 = failed sample
+  unsigned long long* ad_ctrl;
+  long long* ad_redo;       // samples whose fast path missed (recomputed exactly)
 };
 
 struct StateOut {
