@@ -225,6 +225,54 @@ def per_integrator(a, lib, stream, peak):
         torch.cuda.synchronize()
         out[IG_NAME[ig] + "_fp32_state"] = {"path_steps_per_s": 2 * n * (1 << a.level) /
                                             (s.elapsed_time(e) * 1e-3), "paths": n}
+    out["adaptive"] = adaptive_rates(lib, stream)
+    return out
+
+
+def adaptive_rates(lib, stream):
+    """adaptive (non-nested) level 3, defaults (x0 =
+    0.05, u0 = 0.1, T = 1, M0 = 40, x_adapt = 0.05, smoothed indicator); steps
+    actually taken per second on the B200 (2^20 samples) and by the reference's
+    own accumulate_samples on all host threads (bounded sample)."""
+    import numpy as np
+    import torch
+    from paper_1612_07717_b200 import ablmc, capi
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib as O
+    R = O.ref()
+    threads = host_threads()
+    out = {}
+    level = 3
+    for ig in (0, 1, 2):
+        q = ablmc.QoISpec(kind=ablmc.QoIKind.smoothed_indicator)
+        pr = ablmc.Problem.make(ablmc.ModelParams(), ablmc.Integrator(ig), q, 0.05, 0.1, 1.0, 40,
+                                SEED, ablmc.SampleOptions(adaptive=True, x_adapt=0.05))
+        pc = C.byref(pr._c)
+        n = 1 << 20
+        lib.ablmc_accumulate_device(pc, level, 0, n)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        s.record(stream)
+        lib.ablmc_accumulate_device(pc, level, 0, n)
+        e.record(stream)
+        torch.cuda.synchronize()
+        sy, sy2 = np.zeros(1), np.zeros(1)
+        acc = capi.LevelStatsC()
+        acc.level, acc.dim = level, 1
+        acc.sum_y = sy.ctypes.data_as(C.POINTER(C.c_double))
+        acc.sum_y2 = sy2.ctypes.data_as(C.POINTER(C.c_double))
+        lib.ablmc_fetch_device_result(pc, level, C.byref(acc))
+        gpu = acc.cost_steps / (s.elapsed_time(e) * 1e-3)
+        row = {"steps_per_s": gpu, "samples": n, "mean_steps_per_sample": acc.cost_steps / n}
+        if R is not None:
+            st = O.Stats(1)
+            secs = C.c_double()
+            m = 4096 * threads
+            R.ref_accumulate_samples(pc, level, 0, m, threads, C.byref(st.c), C.byref(secs))
+            row["cpu_reference_steps_per_s"] = st.cost_steps / secs.value
+            row["cpu_reference_threads"] = threads
+            row["speedup_vs_cpu_reference"] = gpu / row["cpu_reference_steps_per_s"]
+        out[IG_NAME[ig]] = row
     return out
 
 
