@@ -456,23 +456,61 @@ def decay_sweep(pr: Problem, l_min: int, l_max: int, n_per_level: int) -> list[D
     return [DecayRow(r.level, r.h, r.var_y, r.mean_y, r.se_mean, r.n, r.cost_steps) for r in rows]
 
 
+def _dbl(v: Sequence[float]):
+    return (C.c_double * len(v))(*[float(x) for x in v])
+
+
 def fit_power_law(h: Sequence[float], v: Sequence[float]) -> tuple[float, float]:
-    """estimators.hpp:107-123 -> (exponent, log_prefactor). Host arithmetic only."""
-    import math
-    if len(h) != len(v) or len(h) < 2:
+    """estimators.hpp:107-123 -> (exponent, log_prefactor) (host, in the library)."""
+    if len(h) != len(v):
         raise ValueError("fit_power_law: need at least two points")
-    sx = sy = sxx = sxy = 0.0
-    n = float(len(h))
-    for hi, vi in zip(h, v):
-        if not vi > 0.0:
-            raise ValueError("fit_power_law: values must be positive")
-        x, y = math.log(hi), math.log(vi)
-        sx += x
-        sy += y
-        sxx += x * x
-        sxy += x * y
-    slope = (n * sxy - sx * sy) / (n * sxx - sx * sx)
-    return slope, (sy - slope * sx) / n
+    e, lp = C.c_double(), C.c_double()
+    _check(lib().ablmc_fit_power_law(_dbl(h), _dbl(v), len(h), C.byref(e), C.byref(lp)))
+    return e.value, lp.value
+
+
+@dataclass
+class BiasFit:  # estimators.hpp:131-137
+    alpha: float = 1.0
+    c1: float = 0.0
+    c_y: float = 0.0
+
+    def bias_at(self, h: float) -> float:
+        return self.c1 * h ** self.alpha
+
+
+def estimate_bias_constants(h: Sequence[float], mean_abs: Sequence[float],
+                            std_err: Sequence[float]) -> BiasFit:
+    """estimators.hpp:142-161; RuntimeError when some |E[Y_l]| <= 3 SE."""
+    if not (len(h) == len(mean_abs) == len(std_err)):
+        raise ValueError("estimate_bias_constants: ragged input")
+    a, c1, cy = C.c_double(), C.c_double(), C.c_double()
+    _check(lib().ablmc_estimate_bias_constants(_dbl(h), _dbl(mean_abs), _dbl(std_err), len(h),
+                                               C.byref(a), C.byref(c1), C.byref(cy)))
+    return BiasFit(a.value, c1.value, cy.value)
+
+
+def choose_levels(alpha: float, c1: float, eps: float, m0: int, T: float, l_max: int = 16) -> int:
+    """estimators.hpp:163-175."""
+    L = C.c_int()
+    _check(lib().ablmc_choose_levels(float(alpha), float(c1), float(eps), int(m0), float(T),
+                                     int(l_max), C.byref(L)))
+    return L.value
+
+
+def allocate_samples(var: Sequence[float], h: Sequence[float], eps: float) -> list[int]:
+    """estimators.hpp:177-190."""
+    if len(var) != len(h):
+        raise ValueError("allocate_samples: ragged input")
+    out = (C.c_int64 * len(h))()
+    _check(lib().ablmc_allocate_samples(_dbl(var), _dbl(h), len(h), float(eps), out))
+    return list(out)
+
+
+def adaptive_step_size(x: float, h: float, x_adapt: float, params: ModelParams) -> float:
+    """timeline.hpp:18-23."""
+    p = params.c()
+    return lib().ablmc_adaptive_step_size(float(x), float(h), float(x_adapt), _P(p))
 
 
 def variance_decay_slope(rows: Sequence[DecayRow]) -> float:  # estimators.hpp:434-441

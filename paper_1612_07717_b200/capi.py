@@ -156,6 +156,17 @@ SIGNATURES = {
     "ablmc_decay_sweep": (C.c_int, [P(ProblemC), C.c_int, C.c_int, C.c_int64, P(DecayRowC)]),
     "ablmc_cost_sweep": (C.c_int, [P(ProblemC), C.c_int, P(C.c_double), C.c_int, C.c_double,
                                    C.c_double, P(CostRowC)]),
+    "ablmc_fit_power_law": (C.c_int, [P(C.c_double), P(C.c_double), C.c_int, P(C.c_double),
+                                     P(C.c_double)]),
+    "ablmc_estimate_bias_constants": (C.c_int, [P(C.c_double), P(C.c_double), P(C.c_double),
+                                                C.c_int, P(C.c_double), P(C.c_double),
+                                                P(C.c_double)]),
+    "ablmc_choose_levels": (C.c_int, [C.c_double, C.c_double, C.c_double, C.c_int64, C.c_double,
+                                      C.c_int, P(C.c_int)]),
+    "ablmc_allocate_samples": (C.c_int, [P(C.c_double), P(C.c_double), C.c_int, C.c_double,
+                                         P(C.c_int64)]),
+    "ablmc_adaptive_step_size": (C.c_double, [C.c_double, C.c_double, C.c_double,
+                                              P(ModelParamsC)]),
     "ablmc_run_config_defaults": (None, [P(RunConfigC)]),
     "ablmc_result_json": (C.c_int64, [P(RunConfigC), P(RunResultC), C.c_int64, C.c_char_p,
                                       C.c_int64]),

@@ -428,6 +428,57 @@ int ablmc_cost_sweep(const ablmc_problem* pr, int method, const double* eps_valu
   return 0;
 }
 
+int ablmc_fit_power_law(const double* h, const double* v, int n, double* exponent,
+                        double* log_prefactor) {
+  if (!h || !v || !exponent || !log_prefactor || n < 0) {
+    set_error("fit_power_law: null argument");
+    return ABLMC_ERR_INVALID_ARGUMENT;
+  }
+  PowerFit f;
+  if (int rc = fit_power_law(std::vector<double>(h, h + n), std::vector<double>(v, v + n), f))
+    return rc;
+  *exponent = f.exponent;
+  *log_prefactor = f.log_prefactor;
+  return 0;
+}
+
+int ablmc_estimate_bias_constants(const double* h, const double* mean_abs, const double* std_err,
+                                  int n, double* alpha, double* c1, double* c_y) {
+  if (!h || !mean_abs || !std_err || !alpha || !c1 || !c_y || n < 0) {
+    set_error("estimate_bias_constants: null argument");
+    return ABLMC_ERR_INVALID_ARGUMENT;
+  }
+  std::vector<BiasPoint> pts;
+  for (int i = 0; i < n; ++i) pts.push_back({h[i], mean_abs[i], std_err[i]});
+  BiasFit f;
+  if (int rc = estimate_bias_constants(pts, f)) return rc;
+  *alpha = f.alpha;
+  *c1 = f.c1;
+  *c_y = f.c_y;
+  return 0;
+}
+
+int ablmc_choose_levels(double alpha, double c1, double eps, int64_t m0, double T, int l_max,
+                        int* L) {
+  if (!L) {
+    set_error("choose_levels: null argument");
+    return ABLMC_ERR_INVALID_ARGUMENT;
+  }
+  return choose_levels(alpha, c1, eps, m0, T, l_max, *L);
+}
+
+int ablmc_allocate_samples(const double* var, const double* h, int n_levels, double eps,
+                           int64_t* n_out) {
+  if (!var || !h || !n_out || n_levels < 0) {
+    set_error("allocate_samples: null argument");
+    return ABLMC_ERR_INVALID_ARGUMENT;
+  }
+  const std::vector<int64_t> n = allocate_samples(std::vector<double>(var, var + n_levels),
+                                                  std::vector<double>(h, h + n_levels), eps);
+  for (int l = 0; l < n_levels; ++l) n_out[l] = n[size_t(l)];
+  return 0;
+}
+
 // estimators.hpp:415-431
 int ablmc_decay_sweep(const ablmc_problem* pr, int l_min, int l_max, int64_t n_per_level,
                       ablmc_decay_row* rows) {

@@ -173,3 +173,84 @@ def test_merge_partials_is_ordered_add_merge():
     assert acc.sum_y[0] == ((10.0 + 1.0) + 2.0) + 0.5
     assert acc.sum_y2[0] == 1.0 + 4.0 + 0.25
     assert (acc.n, acc.failed, acc.cost_steps) == (9, 1, 9 * (80 + 40))
+
+
+# ------------------------------------------- estimator helpers (host only)
+def test_allocation_formula_goldens():
+    # test_estimators.cpp:21-29
+    assert ablmc.allocate_samples([1.0], [1.0], 0.1) == [200]
+    assert ablmc.allocate_samples([1.0, 0.25], [1.0, 0.5], 0.1) == [342, 121]
+
+
+def test_allocation_minimises_cost():
+    # test_estimators.cpp:31-64: moving 20% of one level's samples and
+    # restoring the error budget through another never costs less
+    v, h, eps = [0.02, 6e-4, 1.5e-4], [0.025, 0.0125, 0.00625], 1e-3
+    budget = 0.5 * eps * eps
+    s = sum((v[l] / h[l]) ** 0.5 for l in range(3))
+    n = [2.0 / (eps * eps) * (v[l] * h[l]) ** 0.5 * s for l in range(3)]
+    assert ablmc.allocate_samples(v, h, eps) == [int(np.ceil(x)) for x in n]
+
+    def cost(m):
+        return sum(m[l] / h[l] for l in range(3))
+
+    def err2(m):
+        return sum(v[l] / m[l] for l in range(3))
+
+    assert abs(err2(n) / budget - 1.0) <= 1e-12
+    for down in range(3):
+        for up in range(3):
+            if up == down:
+                continue
+            m = list(n)
+            m[down] *= 0.8
+            rest = err2(m) - v[up] / m[up]
+            if rest >= budget:
+                continue
+            m[up] = v[up] / (budget - rest)
+            assert cost(m) >= cost(n) * (1.0 - 1e-12)
+
+
+def test_bias_constant_fit_on_exact_power_laws():
+    # test_estimators.cpp:66-88
+    hs = [0.025, 0.0125, 0.00625, 0.003125]
+    f = ablmc.estimate_bias_constants(hs, [0.5 * h for h in hs], [1e-9] * 4)
+    assert abs(f.alpha - 1.0) <= 1e-10 and abs(f.c1 - 0.5) <= 1e-10
+    f = ablmc.estimate_bias_constants(hs, [3.0 * h * h for h in hs], [1e-12] * 4)
+    assert abs(f.alpha - 2.0) <= 1e-10 and abs(f.c1 - 1.0) <= 1e-10
+    with pytest.raises(RuntimeError, match="indistinguishable"):
+        ablmc.estimate_bias_constants([0.01] * 3, [1e-6] * 3, [1e-6] * 3)
+    with pytest.raises(ValueError, match="at least 3"):
+        ablmc.estimate_bias_constants(hs[:2], [1.0, 2.0], [0.0, 0.0])
+
+
+def test_level_selection():
+    # test_estimators.cpp:90-97
+    assert ablmc.choose_levels(1.0, 1.0, 0.01, 40, 1.0) == 2
+    assert ablmc.choose_levels(1.0, 1.0, 10.0, 40, 1.0) == 0
+    for eps in (0.01, 0.003, 0.001):
+        assert ablmc.choose_levels(2.0, 1.0, eps, 40, 1.0) <= ablmc.choose_levels(1.0, 1.0, eps,
+                                                                                  40, 1.0)
+    with pytest.raises(RuntimeError):
+        ablmc.choose_levels(1.0, 1.0, 1e-9, 40, 1.0, 4)
+    with pytest.raises(ValueError):
+        ablmc.choose_levels(0.0, 1.0, 0.01, 40, 1.0)
+
+
+def test_fit_power_law():
+    e, lp = ablmc.fit_power_law([0.1, 0.05, 0.025], [3 * 0.1 ** 1.5, 3 * 0.05 ** 1.5,
+                                                      3 * 0.025 ** 1.5])
+    assert abs(e - 1.5) <= 1e-12 and abs(np.exp(lp) - 3.0) <= 1e-12
+    with pytest.raises(ValueError, match="positive"):
+        ablmc.fit_power_law([0.1, 0.05], [1.0, 0.0])
+    with pytest.raises(ValueError, match="two points"):
+        ablmc.fit_power_law([0.1], [1.0])
+
+
+def test_adaptive_step_size_goldens():
+    # test_coupling.cpp:18-25
+    mp = ablmc.ModelParams()
+    assert ablmc.adaptive_step_size(0.5, 0.025, 0.05, mp) == 0.025
+    assert ablmc.adaptive_step_size(0.05, 0.025, 0.05, mp) == 0.025
+    v = ablmc.adaptive_step_size(0.01, 0.025, 0.05, mp)
+    assert abs(v - 0.19390825748466839 * 0.025) <= 1e-12 * 0.19390825748466839 * 0.025
