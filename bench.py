@@ -276,6 +276,77 @@ def adaptive_rates(lib, stream):
     return out
 
 
+def _timed_level(lib, stream, pr, level, n, reps=1):
+    """(ms per accumulate call, samples, cost_steps) for one device level."""
+    import numpy as np
+    import torch
+    from paper_1612_07717_b200 import capi
+    pc = C.byref(pr._c)
+    lib.ablmc_accumulate_device(pc, level, 0, n)  # warm-up (workspace growth)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    s.record(stream)
+    for _ in range(reps):
+        lib.ablmc_accumulate_device(pc, level, 0, n)
+    e.record(stream)
+    torch.cuda.synchronize()
+    dim = pr.dim()
+    sy, sy2 = np.zeros(dim), np.zeros(dim)
+    acc = capi.LevelStatsC()
+    acc.level, acc.dim = level, dim
+    acc.sum_y = sy.ctypes.data_as(C.POINTER(C.c_double))
+    acc.sum_y2 = sy2.ctypes.data_as(C.POINTER(C.c_double))
+    lib.ablmc_fetch_device_result(pc, level, C.byref(acc))
+    return s.elapsed_time(e) / reps, acc.n, acc.cost_steps
+
+
+def configs_sweep(lib, stream):
+    """BASELINE.json configs 1, 2 and 4 on one B200 (nondimensional units:
+    H = 1000 m, T = 1000 s, velocities in m/s; DESIGN.md §7 for the
+    extension profiles).  Each level is one device accumulate call of N
+    samples (config 4 bounded to 2^22 paths per level instead of 2e8, to keep
+    the default run short; throughput is per path, so it extrapolates)."""
+    from paper_1612_07717_b200 import ablmc
+    out = {}
+    mp = ablmc.ModelParams()
+    # config 1: homogeneous OU (constant sigma_w = 1.3, tau = 0.1), z0 = H/2,
+    # w0 ~ N(0, sigma_w^2), SE, l = 3 with M_f = 8, N = 1e5, QoI z_T
+    pr = ablmc.Problem.make(mp, ablmc.Integrator.se, ablmc.QoISpec(), 0.5, 0.0, 1.0, 1, SEED,
+                            profile=ablmc.Profile.constant, random_u0=True)
+    ms, n, cost = _timed_level(lib, stream, pr, 3, 100000, reps=20)
+    out["config1_homogeneous_ou_se_l3"] = {"ms_per_level_call": ms, "paths": n,
+                                           "path_steps_per_s": n * 8 / (ms * 1e-3)}
+    # config 2: floored / clamped inhomogeneous profile, w0 ~ N(0, sigma_w(z0)^2),
+    # z0 = H/2, levels 0..8, M0 = 1, N = 1e6 per level, all three integrators
+    c2 = {}
+    for ig in ablmc.Integrator:
+        pr = ablmc.Problem.make(mp, ig, ablmc.QoISpec(), 0.5, 0.0, 1.0, 1, SEED,
+                                profile=ablmc.Profile.floored, random_u0=True)
+        rows = []
+        total_ms = 0.0
+        for level in range(9):
+            ms, n, cost = _timed_level(lib, stream, pr, level, 1000000)
+            total_ms += ms
+            rows.append({"level": level, "ms": ms, "cost_steps": cost})
+        c2[ig.name] = {"levels": rows, "total_ms": total_ms,
+                       "fine_path_steps_per_s_level8": 1e6 * 256 / (rows[-1]["ms"] * 1e-3)}
+    out["config2_floored_levels0to8_1e6"] = c2
+    # config 4: release at z0 = 10 m, 64-bin smoothed concentration field,
+    # GL, levels 0..10, floored profile
+    q = ablmc.QoISpec(kind=ablmc.QoIKind.binned_field, bin_edges=ablmc.equidistant_edges(64, 1.0))
+    pr = ablmc.Problem.make(mp, ablmc.Integrator.gl, q, 0.01, 0.0, 1.0, 1, SEED,
+                            profile=ablmc.Profile.floored, random_u0=True)
+    n4 = 1 << 22
+    rows = []
+    for level in range(11):
+        ms, n, cost = _timed_level(lib, stream, pr, level, n4)
+        rows.append({"level": level, "ms": ms, "paths_per_s": n / (ms * 1e-3)})
+    out["config4_z0_10m_64bins_gl"] = {
+        "paths_per_level": n4, "levels": rows,
+        "projected_seconds_2e8_paths_x_11_levels": sum(2e8 / r["paths_per_s"] for r in rows)}
+    return out
+
+
 def mlmc_sweep(a):
     """BASELINE config 3: full MLMC driver (reference run_mlmc semantics,
     estimators.hpp:284-397) on the reference profile, BAOAB, x0 = 0.5,
@@ -495,6 +566,7 @@ def run_b200(a):
     if not a.no_extras and world == 1:
         line["per_integrator"] = per_integrator(a, lib, stream, fp64_rate.value)
         line["mlmc_time_to_eps"] = mlmc_sweep(a)
+        line["baseline_configs"] = configs_sweep(lib, stream)
     if not a.no_cpu_baseline and world == 1:
         threads = host_threads()
         rate, n_cpu, secs = reference_sample(ig, level, a.cpu_seconds, threads)
