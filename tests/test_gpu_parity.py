@@ -443,3 +443,34 @@ def test_fast_div_sqrt_bit_identical_and_bm_libm_accuracy():
     assert 0 < div_miss < div_n // 4 + div_n // 8 and 0 < sq_miss < sq_n // 4
     assert log_ulp <= 2 and sin_e <= 200 and cos_e <= 200
     assert exp_ulp <= 2 and em1_ulp <= 2 and em2_ulp <= 3
+
+
+def test_full_size_c5_properties():
+    """BASELINE config 5 at the bench's full size (2^25 coupled paths, level 10,
+    SE, reference profile): size-independent properties the oracle cannot
+    check at this size -- exact counts and cost, bit-identical sums for one
+    call vs an 8-way super-block split merged in order vs a rerun (the
+    multi-GPU contract), and the coupled level's variance ratio to level 9
+    near the strong-order-1/2 value 2^-1 ... 2^-2 band (Var[Y_l] ~ h^beta,
+    beta in [1, 2])."""
+    pr = ablmc.Problem.make(ablmc.ModelParams(), Ig.se, ablmc.QoISpec(), 0.5, 0.1, 1.0, 1, 42)
+    n = 1 << 25
+    one = ablmc.LevelStats().init(10, pr.h_level(10), 1)
+    ablmc.accumulate_samples(one, 0, n, pr, 10)
+    assert (one.n, one.failed, one.cost_steps) == (n, 0, n * (1024 + 512))
+    again = ablmc.LevelStats().init(10, pr.h_level(10), 1)
+    ablmc.accumulate_samples(again, 0, n, pr, 10)
+    assert (again.sum_y[0], again.sum_y2[0]) == (one.sum_y[0], one.sum_y2[0])
+    nsb = ablmc.num_superblocks(n)
+    assert nsb == 8
+    parts = [ablmc.accumulate_partials(pr, 10, 0, n, k, k + 1) for k in range(nsb)]
+    acc = ablmc.LevelStats().init(10, pr.h_level(10), 1)
+    ablmc.merge_partials(acc, pr, 10, np.concatenate([p[0] for p in parts]),
+                         np.concatenate([p[1] for p in parts]))
+    assert (acc.sum_y[0], acc.sum_y2[0], acc.n, acc.cost_steps) == (
+        one.sum_y[0], one.sum_y2[0], one.n, one.cost_steps)
+    l9 = ablmc.LevelStats().init(9, pr.h_level(9), 1)
+    ablmc.accumulate_samples(l9, 0, n // 4, pr, 9)
+    ratio = one.variance() / l9.variance()
+    assert 0.2 < ratio < 0.55, ratio
+    assert abs(one.mean()) < 6 * one.std_error() + 1e-4  # E[Y_10] ~ c h: tiny
