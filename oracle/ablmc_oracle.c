@@ -90,8 +90,58 @@ static double clamp_height(double x, const ablmc_model_params* p) {
   return (x < lo) ? lo : (hi < x) ? hi : x;
 }
 
+/* Extension profiles (NOT in the reference; BASELINE.json configs 1-5 as
+ * written): restated from this project's definition in
+ * paper_1612_07717_b200/csrc/ablmc_device.cuh coeffs<PROF>, so the device
+ * extension paths have a checker.  Selected per thread by orc_set_profile
+ * (orc_accumulate_* set it from the problem). */
+typedef struct {
+  int profile; /* ABLMC_PROFILE_* */
+  double const_sigma_u, const_tau, sigma_floor, tau_min, tau_max;
+} orc_profile;
+static __thread orc_profile g_prof = {0, 0, 0, 0, 0, 0};
+
+void orc_set_profile(int profile, double const_sigma_u, double const_tau, double sigma_floor,
+                     double tau_min, double tau_max) {
+  g_prof.profile = profile;
+  g_prof.const_sigma_u = const_sigma_u;
+  g_prof.const_tau = const_tau;
+  g_prof.sigma_floor = sigma_floor;
+  g_prof.tau_min = tau_min;
+  g_prof.tau_max = tau_max;
+}
+
+static orc_coeffs ext_coeffs(double x, const ablmc_model_params* p) {
+  orc_coeffs c;
+  if (g_prof.profile == ABLMC_PROFILE_CONSTANT) { /* D1: homogeneous OU */
+    const double su2 = g_prof.const_sigma_u * g_prof.const_sigma_u;
+    const double lam = 1.0 / g_prof.const_tau;
+    c.sigma_u2 = su2;
+    c.lambda = lam;
+    c.sigma = p->noise_scale * sqrt(2.0 * su2 * lam);
+    c.dsigma_u2 = 0.0;
+    return c;
+  }
+  /* D3: sigma_U floored, tau = kappa_tau x / sigma_U clamped to [tau_min, tau_max] */
+  const double xc = fmin(fmax(x, 0.0), p->H);
+  const double t = 1.0 - xc / p->H;
+  const double st = sqrt(t);
+  const double su_raw = (p->kappa_sigma * p->u_star) * sqrt(t * st);
+  const int floored = !(su_raw > g_prof.sigma_floor);
+  const double su = floored ? g_prof.sigma_floor : su_raw;
+  double tau = (p->kappa_tau * xc) / su;
+  tau = fmin(fmax(tau, g_prof.tau_min), g_prof.tau_max);
+  const double a = p->kappa_sigma * p->u_star;
+  c.sigma_u2 = su * su;
+  c.lambda = 1.0 / tau;
+  c.sigma = p->noise_scale * sqrt(2.0 * c.sigma_u2 * c.lambda);
+  c.dsigma_u2 = floored ? 0.0 : (-1.5 * a * a * st) / p->H;
+  return c;
+}
+
 /* model.hpp:73-89 */
 orc_coeffs orc_sde_coeffs(double x, const ablmc_model_params* p) {
+  if (g_prof.profile != ABLMC_PROFILE_REFERENCE) return ext_coeffs(x, p);
   const double xc = clamp_height(x, p);
   const double a = p->kappa_sigma * p->u_star;
   const double t = 1.0 - xc / p->H;
@@ -475,16 +525,25 @@ static int64_t one_sample(const ablmc_problem* pr, const double* poly, int coupl
                           int64_t M, uint32_t stream_level, int64_t idx, double* y,
                           double* scratch) {
   const ablmc_model_params* p = &pr->params;
+  double u0 = pr->u0;
+  if (pr->random_u0) {
+    /* Extension D2 (not in the reference): u0 = sigma_U(x0) z with z = draw
+     * k = M of the sample's stream, shared by fine and coarse (device
+     * run_sample). */
+    const double z = orc_normal_at(pr->seed, coupled ? (uint32_t)level : stream_level,
+                                   (uint64_t)idx, (uint64_t)M);
+    u0 = sqrt(orc_sde_coeffs(pr->x0, p).sigma_u2) * z;
+  }
   if (coupled) {
     orc_state f, c;
     int64_t steps = M + M / 2;
     int rc;
     if (pr->adaptive) /* coupling.hpp:262-265 */
-      rc = orc_simulate_pair_adaptive(pr->integrator, p, pr->x0, pr->u0, pr->T, pr->T / (double)M,
+      rc = orc_simulate_pair_adaptive(pr->integrator, p, pr->x0, u0, pr->T, pr->T / (double)M,
                                       pr->x_adapt, pr->seed, (uint32_t)level, (uint64_t)idx,
                                       NULL, pr->signs_on, &f, &c, &steps);
     else
-      rc = orc_simulate_pair(pr->integrator, p, pr->x0, pr->u0, pr->T, M, pr->seed,
+      rc = orc_simulate_pair(pr->integrator, p, pr->x0, u0, pr->T, M, pr->seed,
                              (uint32_t)level, (uint64_t)idx, NULL, pr->signs_on, &f, &c);
     if (rc) return -1;
     orc_evaluate(&pr->qoi, poly, pr->qoi.r, f.x, y);
@@ -497,11 +556,11 @@ static int64_t one_sample(const ablmc_problem* pr, const double* poly, int coupl
   int64_t steps = M;
   int rc;
   if (pr->adaptive) /* coupling.hpp:238-240 */
-    rc = orc_simulate_path_adaptive(pr->integrator, p, pr->x0, pr->u0, pr->T, pr->T / (double)M,
+    rc = orc_simulate_path_adaptive(pr->integrator, p, pr->x0, u0, pr->T, pr->T / (double)M,
                                     pr->x_adapt, pr->seed, stream_level, (uint64_t)idx, NULL, &s,
                                     &steps);
   else
-    rc = orc_simulate_path(pr->integrator, p, pr->x0, pr->u0, pr->T, M, pr->seed, stream_level,
+    rc = orc_simulate_path(pr->integrator, p, pr->x0, u0, pr->T, M, pr->seed, stream_level,
                            (uint64_t)idx, NULL, &s);
   if (rc) return -1;
   orc_evaluate(&pr->qoi, poly, pr->qoi.r, s.x, y);
@@ -514,6 +573,8 @@ static int accumulate(const ablmc_problem* pr, int coupled, int level, int64_t M
                       uint32_t stream_level, int64_t first, int64_t count,
                       ablmc_level_stats* acc) {
   if (count <= 0) return 0;
+  orc_set_profile(pr->profile, pr->const_sigma_u, pr->const_tau, pr->sigma_floor, pr->tau_min,
+                  pr->tau_max);
   double poly[14] = {0};
   if (orc_build_smoothing_polynomial(pr->qoi.r, poly)) return -1;
   const int64_t dim = qoi_dim(&pr->qoi);
@@ -550,6 +611,7 @@ static int accumulate(const ablmc_problem* pr, int coupled, int level, int64_t M
     acc->cost_steps += pc;
   }
   free(y);
+  orc_set_profile(ABLMC_PROFILE_REFERENCE, 0, 0, 0, 0, 0);
   return 0;
 }
 

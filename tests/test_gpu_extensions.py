@@ -1,7 +1,9 @@
 """GPU tests of (1) the IEEE-only kernel path and the fast path's recompute
 on a fast-path miss, and (2) the extensions BASELINE.json asks for that the
 reference cannot express — parity unpinned vs the
-reference: analytic and statistical checks only."""
+reference (which has no such modes): analytic and statistical checks, plus
+sample-by-sample parity with the C oracle's restatement of the extension
+definitions (orc_set_profile, random u0 in orc_accumulate_*)."""
 import ctypes as C
 
 import numpy as np
@@ -128,3 +130,68 @@ def test_random_u0_coupled_levels_decay():
         v.append(st.variance())
     slope = np.polyfit(np.log([1 / 8, 1 / 16, 1 / 32, 1 / 64]), np.log(v), 1)[0]
     assert 1.6 < slope < 2.4
+
+
+EXT = {"constant": dict(profile=ablmc.Profile.constant, const_sigma_u=1.3, const_tau=0.1),
+       "floored": dict(profile=ablmc.Profile.floored, sigma_floor=1e-3, tau_min=1e-5,
+                       tau_max=1.0)}
+
+
+def set_oracle_profile(pr):
+    c = pr._c
+    O.orc().orc_set_profile(c.profile, c.const_sigma_u, c.const_tau, c.sigma_floor, c.tau_min,
+                            c.tau_max)
+
+
+@pytest.mark.parametrize("prof", ["constant", "floored"])
+@pytest.mark.parametrize("ig", list(Ig))
+def test_extension_profiles_oracle_mode_vs_oracle(prof, ig):
+    """D1/D3 pairs with host-supplied normals against the oracle's restatement
+    of the extension profiles: SE bit-identical, GL/BAOAB within rel 1e-12
+    (device exp/expm1), parities / reflection counts / ok flags exact."""
+    rng = np.random.default_rng(23)
+    x0, T, m0, level, n = 0.3, 1.0, 16, 3, 48
+    if prof == "constant" and ig == Ig.se:
+        m0 = 64  # lambda = 10: SE needs h < 0.2 at the coarse step
+    pr = ablmc.Problem.make(ablmc.ModelParams(), ig, ablmc.QoISpec(), x0, 0.1, T, m0, 9,
+                            **EXT[prof])
+    M = m0 << level
+    xi = rng.normal(size=(n, M))
+    got = ablmc.simulate_pairs(pr, level, 0, n, xi=xi)
+    set_oracle_profile(pr)
+    try:
+        p = O.default_params()
+        for i in range(n):
+            rc, f, c = O.orc_pair(int(ig), p, x0, 0.1, T, M, 9, level, i, xi=xi[i])
+            assert (rc == 0) == bool(got["fok"][i]), i
+            if rc:
+                continue
+            g = got[i]
+            assert (g["fpar"], g["fn"], g["cpar"], g["cn"]) == (f.parity, f.n_refl, c.parity,
+                                                                c.n_refl), i
+            v, w = [g["fx"], g["fu"], g["cx"], g["cu"]], [f.x, f.u, c.x, c.u]
+            if ig == Ig.se:
+                assert v == w, i
+            else:
+                assert np.allclose(v, w, rtol=1e-12, atol=1e-13), i
+    finally:
+        O.orc().orc_set_profile(0, 0, 0, 0, 0, 0)
+
+
+@pytest.mark.parametrize("prof", ["reference", "constant", "floored"])
+@pytest.mark.parametrize("level", [0, 2])
+def test_random_u0_and_profiles_accumulate_vs_oracle(prof, level):
+    """D2 (w0 ~ N(0, sigma_U(x0)^2) from draw k = M of the sample's stream)
+    with each profile: level sums against the oracle's accumulate on the same
+    Philox streams (Box-Muller within ulps of glibc): counts and cost exact,
+    sums within rel 1e-10."""
+    kw = EXT.get(prof, {})
+    pr = ablmc.Problem.make(ablmc.ModelParams(), Ig.gl, ablmc.QoISpec(), 0.5, 0.0, 1.0, 8, 11,
+                            random_u0=True, **kw)
+    acc = ablmc.LevelStats().init(level, pr.h_level(level), 1)
+    ablmc.accumulate_samples(acc, 5, 20000, pr, level)
+    st = O.Stats(1)
+    assert O.orc().orc_accumulate_samples(C.byref(pr._c), level, 5, 20000, C.byref(st.c)) == 0
+    assert (acc.n, acc.failed, acc.cost_steps) == (st.n, st.failed, st.cost_steps)
+    assert abs(acc.sum_y[0] - st.sum_y[0]) <= 1e-10 * abs(st.sum_y[0]) + 1e-12
+    assert abs(acc.sum_y2[0] - st.sum_y2[0]) <= 1e-10 * abs(st.sum_y2[0]) + 1e-12
