@@ -570,10 +570,12 @@ def run_b200(a):
     if not a.no_cpu_baseline and world == 1:
         threads = host_threads()
         rate, n_cpu, secs = reference_sample(ig, level, a.cpu_seconds, threads)
+        rate1, n1, secs1 = reference_sample(ig, level, 3.0, 1)  # also 1 thread
         line["cpu_baseline"] = {"value": rate, "unit": "path-steps/s", "cores": threads,
                                 "kind": "reference",
                                 "sample": f"{n_cpu} coupled paths x {Mf} fine steps in {secs:.1f} s, "
-                                          f"reference accumulate_samples, {threads} threads"}
+                                          f"reference accumulate_samples, {threads} threads",
+                                "single_thread": {"value": rate1, "paths": n1, "seconds": secs1}}
     print(json.dumps(line), flush=True)
     if dist_on:
         dist.barrier()
