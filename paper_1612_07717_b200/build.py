@@ -16,7 +16,8 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OBJ = PKG / "build"
 LIB = PKG / "libablmc_b200.so"
-SOURCES = ["level_kernels.cu", "capi.cu", "drivers.cu", "output.cpp"]
+SOURCES = ["level_kernels.cu", "adaptive_kernels.cu", "binned_kernels.cu", "capi.cu", "drivers.cu",
+           "output.cpp"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = os.environ.get("CXX", "g++")
@@ -50,7 +51,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
                 cmd = [CXX, *CXXFLAGS, "-c", str(s), "-o", str(o)]
             else:
                 cmd = [NVCC, *ARCH, *FLAGS, "-c", str(s), "-o", str(o)]
-            if src == "level_kernels.cu":
+            if src.endswith("_kernels.cu"):
                 cmd += ["-Xptxas", "-v"]
             jobs.append((cmd, o))
 

@@ -74,6 +74,12 @@ cudaError_t launch_level(const KernelArgs& a, int ig, bool coupled, double* tile
                          long long* tile_cnt, cudaStream_t st);
 cudaError_t launch_states(const KernelArgs& a, int ig, bool coupled, const double* xi,
                           StateOut* out, cudaStream_t st);
+// adaptive_kernels.cu / binned_kernels.cu (called by launch_level / launch_states)
+cudaError_t launch_adaptive_level(const KernelArgs& a, int ig, bool coupled, double* tile_sums,
+                                  long long* tile_cnt, cudaStream_t st);
+cudaError_t launch_adaptive_states(const KernelArgs& a, int ig, bool coupled, StateOut* out,
+                                   cudaStream_t st);
+cudaError_t launch_binned(const KernelArgs& a, bool coupled, double* tile_sums, cudaStream_t st);
 cudaError_t launch_merge_tiles(int64_t n_tiles, int dim, const double* ts, const long long* tc,
                                double* bs, long long* bc, cudaStream_t st);
 cudaError_t launch_merge_blocks(int64_t n_blk, int dim, const double* bs, const long long* bc,

@@ -1,0 +1,260 @@
+// level_common.cuh — device pieces shared by the level-sampler kernels
+// (level_kernels.cu, adaptive_kernels.cu, binned_kernels.cu): the
+// uniform-grid sampler, the QoI evaluation and the fixed-tree tile
+// reduction.  Internal linkage: each translation unit gets its own copy.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "ablmc_device.cuh"
+#include "kernels.h"
+
+namespace {
+
+using namespace ablmc_dev;
+
+constexpr int kTile = ABLMC_TILE;            // samples per CTA (one per thread)
+constexpr int kWarps = kTile / 32;
+
+struct PathOut {
+  PState f, c;
+  bool ok;
+};
+
+// simulate_pair (coupling.hpp:64-105) / simulate_path (coupling.hpp:22-29)
+// for one sample.  XI: read normals from xi (oracle mode) instead of Philox.
+// FAST: fast div/sqrt; returns early with bad = true on any fast-path miss
+// (the caller then recomputes the sample with FAST = false).
+template <int IG, int PROF, bool COUPLED, bool XI, int FAST>
+__device__ __forceinline__ PathOut run_sample(const KernelArgs& a, uint64_t idx,
+                                              const double* __restrict__ xi, bool& bad) {
+  const DevModel& m = a.model;
+  PathOut o;
+  double u0 = a.u0;
+  if (a.random_u0) {
+    // Extension D2: u0 ~ N(0, sigma_U(x0)^2) from draw k = M of this stream
+    // (disjoint from the step draws 0..M-1), shared by fine and coarse.
+    double z0, z1;
+    normal_pair(uint64_t(a.M) >> 1, idx, a.key, z0, z1);
+    const double z = (a.M & 1) ? z1 : z0;
+    u0 = mul(__dsqrt_rn(coeffs<PROF, false>(a.x0, m, bad).su2), z);
+  }
+  o.f = {a.x0, u0, 1, 0};
+  o.c = o.f;
+  o.ok = true;
+  const double h = a.h, sqrt_h = a.sqrt_h;
+  if (!COUPLED) {
+    Coef c0;
+    if (IG == kBAOAB) c0 = coeffs<PROF, FAST>(a.x0, m, bad);
+    double z0 = 0.0, z1 = 0.0;
+    for (int64_t k = 0; k < a.M; ++k) {
+      double xi_k;
+      if (XI) {
+        xi_k = xi[k];
+      } else {
+        if ((k & 1) == 0) normal_pair(uint64_t(k) >> 1, idx, a.key, z0, z1);
+        xi_k = (k & 1) ? z1 : z0;
+      }
+      bool ok;
+      if (IG == kSE) {
+        ok = se_step<PROF, FAST>(o.f, h, sqrt_h, xi_k, m, bad);
+      } else if (IG == kGL) {
+        double e;
+        ok = gl_step<PROF, FAST>(o.f, h, xi_k, m, e, bad);
+      } else {
+        int pm;
+        ok = baoab_step<PROF, FAST>(o.f, c0, h, a.h_half, xi_k, false, pm, m, bad);
+      }
+      if (!ok) o.ok = false;
+      if (!ok || (FAST && bad)) break;
+    }
+    return o;
+  }
+  const double h2 = a.h2, sqrt_h2 = a.sqrt_h2;
+  const bool signs = a.signs_on;
+  Coef cf, cc;  // BAOAB: cached sde_coeffs at the current fine / coarse x
+  if (IG == kBAOAB) {
+    cf = coeffs<PROF, FAST>(a.x0, m, bad);
+    cc = cf;
+  }
+  const int64_t windows = a.M >> 1;
+  // (Generating the normals one window ahead was measured 12% slower: the
+  // scheduler already overlaps Box-Muller with the window's steps, and the
+  // extra live registers cost occupancy.)
+  for (int64_t n = 0; n < windows; ++n) {
+    double xi0, xi1;
+    if (XI) {
+      xi0 = xi[2 * n];
+      xi1 = xi[2 * n + 1];
+    } else {
+      normal_pair(uint64_t(n), idx, a.key, xi0, xi1);
+    }
+    bool ok;
+    if (IG == kSE) {
+      const int p0 = o.f.par;
+      ok = se_step<PROF, FAST>(o.f, h, sqrt_h, xi0, m, bad);
+      const int p1 = o.f.par;
+      ok = ok && se_step<PROF, FAST>(o.f, h, sqrt_h, xi1, m, bad);
+      const int s0 = signs ? p0 : 1, s1 = signs ? p1 : 1, sc = signs ? o.c.par : 1;
+      ok = ok && se_step<PROF, FAST>(o.c, h2, sqrt_h2,
+                                     coarse_noise_se<FAST>(xi0, xi1, s0, s1, sc, bad), m, bad);
+    } else if (IG == kGL) {
+      const int p0 = o.f.par;
+      double e0, e1, ec;
+      ok = gl_step<PROF, FAST>(o.f, h, xi0, m, e0, bad);  // e0 = exp(-lam(x_f at window start) h)
+      const int p1 = o.f.par;
+      ok = ok && gl_step<PROF, FAST>(o.f, h, xi1, m, e1, bad);
+      const int s0 = signs ? p0 : 1, s1 = signs ? p1 : 1, sc = signs ? o.c.par : 1;
+      ok = ok && gl_step<PROF, FAST>(o.c, h2, coarse_noise_gl_e<FAST>(xi0, xi1, e0, s0, s1, sc, bad),
+                                     m, ec, bad);
+    } else {
+      const double e = ou_decay<FAST>(cf.lam, h, bad);  // lam_fine at the window start
+      int pm0, pm1, pmc;
+      ok = baoab_step<PROF, FAST>(o.f, cf, h, a.h_half, xi0, false, pm0, m, bad);
+      ok = ok && baoab_step<PROF, FAST>(o.f, cf, h, a.h_half, xi1, false, pm1, m, bad);
+      const int s0 = signs ? pm0 : 1, s1 = signs ? pm1 : 1;
+      ok = ok && baoab_step<PROF, FAST>(o.c, cc, h2, a.h2_half,
+                                        coarse_noise_gl_e<FAST>(xi0, xi1, e, s0, s1, 1, bad),
+                                        signs, pmc, m, bad);
+    }
+    if (!ok) o.ok = false;
+    if (!ok || (FAST && bad)) break;
+  }
+  return o;
+}
+
+// One sample with IEEE-exact div/sqrt semantics: the fast variant when the
+// host certified tame parameters, recomputed with the IEEE variant on a
+// fast-path miss.
+template <int IG, int PROF, bool COUPLED, bool XI>
+__device__ __forceinline__ PathOut sample(const KernelArgs& a, uint64_t idx,
+                                          const double* __restrict__ xi) {
+  bool bad = false;
+  if (a.fast) {
+    PathOut o = a.fast == kFastUnit ? run_sample<IG, PROF, COUPLED, XI, kFastUnit>(a, idx, xi, bad)
+                                    : run_sample<IG, PROF, COUPLED, XI, 1>(a, idx, xi, bad);
+    if (!bad) return o;
+    bad = false;
+  }
+  return run_sample<IG, PROF, COUPLED, XI, 0>(a, idx, xi, bad);
+}
+
+// ----------------------------------------------------------------- QoI
+// qoi.hpp:22-26 Horner, 80-84 g_r.
+__device__ __forceinline__ double g_r(double s, const KernelArgs& a) {
+  if (s < -1.0) return 1.0;
+  if (s > 1.0) return 0.0;
+  double acc = 0.0;
+  for (int i = a.poly_n; i-- > 0;) acc = add(mul(acc, s), a.poly[i]);
+  return acc;
+}
+
+// qoi.hpp:171-188 for the scalar kinds.
+__device__ __forceinline__ double qoi_scalar(double x, const KernelArgs& a) {
+  switch (a.qoi_kind) {
+    case 0: return x;
+    case 2: return (x >= a.qa && x <= a.qb) ? 1.0 : 0.0;
+    case 1: return sub(g_r(__ddiv_rn(sub(x, a.qb), a.delta), a), g_r(__ddiv_rn(sub(x, a.qa), a.delta), a));
+    default: return 0.0;
+  }
+}
+
+// binned_field g-term at edge e (qoi.hpp:157-167): g_r((x - edge[e]) / delta)
+// with the pinned values g(edge 0) = 0 and g(edge k) = 1.
+__device__ __forceinline__ double g_edge(double x, int e, int k, const double* edges,
+                                         const KernelArgs& a) {
+  if (e == 0) return 0.0;
+  if (e == k) return 1.0;
+  return g_r(__ddiv_rn(sub(x, edges[e]), a.delta), a);
+}
+
+// Resident CTAs per SM requested from ptxas (register budget 65536 / (256 *
+// blocks)); tuned per integrator against spills.
+template <int IG>
+struct MinBlocks {
+  static constexpr int value = IG == kSE ? ABLMC_MINB_SE : (IG == kGL ? ABLMC_MINB_GL : ABLMC_MINB_BAOAB);
+};
+
+// Tile reduction shared by the level kernels: the tile's {sum_y, sum_y2}
+// (fixed warp-shuffle tree, then warps in order) of the successful samples'
+// QoI values y, and counts {n, failed, cost_steps}.  Binned field: sums come
+// from K4, only the counts are reduced here.
+__device__ __forceinline__ void tile_reduce(bool active, bool good, double y, long long steps,
+                                            bool binned, double* __restrict__ tile_sums,
+                                            long long* __restrict__ tile_cnt) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ double s_red[kWarps][2];
+  __shared__ long long s_cnt[kWarps][kCnt];
+  long long cn = good ? 1 : 0, cf = (active && !good) ? 1 : 0, cc = good ? steps : 0;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    cn += __shfl_down_sync(0xffffffffu, cn, off);
+    cf += __shfl_down_sync(0xffffffffu, cf, off);
+    cc += __shfl_down_sync(0xffffffffu, cc, off);
+  }
+  if (lane == 0) {
+    s_cnt[warp][0] = cn;
+    s_cnt[warp][1] = cf;
+    s_cnt[warp][2] = cc;
+  }
+  if (!binned) {
+    double sy = good ? y : 0.0, sy2 = good ? mul(y, y) : 0.0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      sy = add(sy, __shfl_down_sync(0xffffffffu, sy, off));
+      sy2 = add(sy2, __shfl_down_sync(0xffffffffu, sy2, off));
+    }
+    if (lane == 0) {
+      s_red[warp][0] = sy;
+      s_red[warp][1] = sy2;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double ty = 0.0, ty2 = 0.0;
+    long long t[kCnt] = {0, 0, 0};
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      ty = add(ty, s_red[w][0]);
+      ty2 = add(ty2, s_red[w][1]);
+      for (int c = 0; c < kCnt; ++c) t[c] += s_cnt[w][c];
+    }
+    if (!binned) {
+      tile_sums[2 * blockIdx.x] = ty;  // dim == 1
+      tile_sums[2 * blockIdx.x + 1] = ty2;
+    }
+    for (int c = 0; c < kCnt; ++c) tile_cnt[kCnt * blockIdx.x + c] = t[c];
+  }
+}
+
+// QoI value of one successful sample (qoi.hpp:171-188; the difference for a
+// coupled pair, coupling.hpp:262-268).
+template <bool COUPLED>
+__device__ __forceinline__ double sample_y(const KernelArgs& a, const PathOut& o) {
+  double y = qoi_scalar(o.f.x, a);
+  if (COUPLED) y = sub(y, qoi_scalar(o.c.x, a));
+  return y;
+}
+
+// binned field: the terminal positions for K4 (failed samples as NaN: K4
+// skips them).
+__device__ __forceinline__ void store_pos(const KernelArgs& a, int64_t j, bool good,
+                                          const PathOut& o) {
+  a.pos[2 * j] = good ? o.f.x : __longlong_as_double(0x7ff8000000000000LL);
+  a.pos[2 * j + 1] = o.c.x;
+}
+
+// Tile epilogue of the one-thread-per-sample kernels.
+template <bool COUPLED>
+__device__ __forceinline__ void tile_epilogue(const KernelArgs& a, int64_t j, bool active,
+                                              const PathOut& o, long long steps,
+                                              double* __restrict__ tile_sums,
+                                              long long* __restrict__ tile_cnt) {
+  const bool good = active && o.ok;
+  const bool binned = a.qoi_kind == 3;
+  if (binned && active) store_pos(a, j, good, o);
+  tile_reduce(active, good, (!binned && good) ? sample_y<COUPLED>(a, o) : 0.0, steps, binned,
+              tile_sums, tile_cnt);
+}
+
+}  // namespace
