@@ -341,6 +341,12 @@ def configs_sweep(lib, stream):
     for level in range(11):
         ms, n, cost = _timed_level(lib, stream, pr, level, n4)
         rows.append({"level": level, "ms": ms, "paths_per_s": n / (ms * 1e-3)})
+    # config 5 throughput against N (the headline runs 2^25 per GPU)
+    pr = ablmc.Problem.make(mp, ablmc.Integrator.se, ablmc.QoISpec(), 0.5, 0.1, 1.0, 1, SEED)
+    out["config5_se_l10_n_sweep"] = {}
+    for n in (10**6, 10**7, 10**8):
+        ms, ok, cost = _timed_level(lib, stream, pr, 10, n)
+        out["config5_se_l10_n_sweep"][f"{n:.0e}"] = {"ms": ms, "path_steps_per_s": ok * 1024 / (ms * 1e-3)}
     out["config4_z0_10m_64bins_gl"] = {
         "paths_per_level": n4, "levels": rows,
         "projected_seconds_2e8_paths_x_11_levels": sum(2e8 / r["paths_per_s"] for r in rows)}
