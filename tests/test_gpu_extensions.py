@@ -195,3 +195,30 @@ def test_random_u0_and_profiles_accumulate_vs_oracle(prof, level):
     assert (acc.n, acc.failed, acc.cost_steps) == (st.n, st.failed, st.cost_steps)
     assert abs(acc.sum_y[0] - st.sum_y[0]) <= 1e-10 * abs(st.sum_y[0]) + 1e-12
     assert abs(acc.sum_y2[0] - st.sum_y2[0]) <= 1e-10 * abs(st.sum_y2[0]) + 1e-12
+
+
+@pytest.mark.parametrize("prof", ["constant", "floored"])
+def test_extension_profiles_adaptive_se_bit_exact(prof):
+    """Adaptive stepping on the extension profiles: SE pairs bit-identical to
+    the oracle driven by the device's own normal stream (the adaptive
+    schedule is ulp-sensitive, see tests/test_gpu_adaptive.py)."""
+    m0 = 64 if prof == "constant" else 20
+    pr = ablmc.Problem.make(ablmc.ModelParams(), Ig.se, ablmc.QoISpec(), 0.3, 0.1, 1.0, m0, 13,
+                            ablmc.SampleOptions(adaptive=True, x_adapt=0.2), **EXT[prof])
+    level, n = 2, 64
+    M = m0 << level
+    got = ablmc.simulate_pairs(pr, level, 0, n)
+    set_oracle_profile(pr)
+    try:
+        p = O.default_params()
+        for i in range(n):
+            xi = ablmc.normals(13, level, i, 0, 256 * M + 257)
+            rc, f, c, steps = O.orc_pair_adaptive(0, p, 0.3, 0.1, 1.0, 1.0 / M, 0.2, 13, level, i,
+                                                  1, xi=xi)
+            assert (rc == 0) == bool(got["fok"][i]), i
+            if rc == 0:
+                g = got[i]
+                assert [g["fx"], g["fu"], g["cx"], g["cu"]] == [f.x, f.u, c.x, c.u], i
+                assert (g["fn"], g["cn"]) == (f.n_refl, c.n_refl)
+    finally:
+        O.orc().orc_set_profile(0, 0, 0, 0, 0, 0)
