@@ -56,6 +56,110 @@ double orc_bits_to_unit(uint32_t hi, uint32_t lo) {
   return ((double)(b >> 11) + 0.5) * 0x1.0p-53;
 }
 
+
+/* ---------------------------------------------------- device-math mode
+ * NOT the reference: a restatement of this project's device elementary
+ * functions (paper_1612_07717_b200/csrc/ablmc_device.cuh log_unit,
+ * sincos_2pi, expm1_exp_core and the expm1(2x) = em1 (em1 + 2) identity),
+ * with the same explicit FMAs, so tests can drive the oracle with the
+ * device's exact log/sin/cos/exp/expm1 and require bit-identical paths for
+ * every integrator.  The reference's own math (glibc) stays the default. */
+static __thread int g_devmath = 0;
+void orc_set_device_math(int on) { g_devmath = on; }
+
+static uint64_t dbits(double v) { uint64_t b; memcpy(&b, &v, 8); return b; }
+static double bitsd(uint64_t b) { double v; memcpy(&v, &b, 8); return v; }
+static int lo_int(double v) { return (int)(int32_t)(uint32_t)dbits(v); }
+
+static const double kLg[7] = {6.666666666666735130e-01, 3.999999999940941908e-01,
+                              2.857142874366239149e-01, 2.222219843214978396e-01,
+                              1.818357216161805012e-01, 1.531383769920937332e-01,
+                              1.479819860511658591e-01};
+static const double kS[6] = {-1.66666666666666324348e-01, 8.33333333332248946124e-03,
+                             -1.98412698298579493134e-04, 2.75573137070700676789e-06,
+                             -2.50507602534068634195e-08, 1.58969099521155010221e-10};
+static const double kC[6] = {4.16666666666666019037e-02, -1.38888888888741095749e-03,
+                             2.48015872894767294178e-05, -2.75573143513906633035e-07,
+                             2.08757232129817482790e-09, -1.13596475577881948265e-11};
+static const double kBm[6] = {6.93147180369123816490e-01, 1.90821492927058770002e-10,
+                              6.36619772367581382433e-01, 1.57079632673412561417e+00,
+                              6.07710050650619224932e-11, 6755399441055744.0};
+static const double kEP[12] = {1.0 / 2, 1.0 / 6, 1.0 / 24, 1.0 / 120, 1.0 / 720, 1.0 / 5040,
+                               1.0 / 40320, 1.0 / 362880, 1.0 / 3628800, 1.0 / 39916800,
+                               1.0 / 479001600, 1.0 / 6227020800.0};
+static const double kER[4] = {1.44269504088896338700e+00, 6.93147180369123816490e-01,
+                              1.90821492927058770002e-10, 6755399441055744.0};
+
+static double dm_log_unit(double u) {
+  const uint64_t b = dbits(u);
+  int32_t hx = (int32_t)(b >> 32);
+  int k = (hx >> 20) - 1023;
+  hx &= 0x000fffff;
+  const int i = (hx + 0x95f64) & 0x100000;
+  const double mnt = bitsd(((uint64_t)(uint32_t)(hx | (i ^ 0x3ff00000)) << 32) | (uint32_t)b);
+  k += i >> 20;
+  const double f = mnt - 1.0;
+  const double hfsq = (0.5 * f) * f;
+  const double sq = f / (2.0 + f);
+  const double z = sq * sq;
+  const double w = z * z;
+  const double p1 = fma(w, fma(w, kLg[5], kLg[3]), kLg[1]);
+  const double t2 = z * fma(w, fma(w, fma(w, kLg[6], kLg[4]), kLg[2]), kLg[0]);
+  const double R = fma(w, p1, t2);
+  const double dk = (double)k;
+  const double inner = fma(sq, hfsq + R, dk * kBm[1]);
+  return fma(dk, kBm[0], -((hfsq - inner) - f));
+}
+
+static void dm_sincos_2pi(double th, double* sn, double* cs) {
+  const double t = fma(th, kBm[2], kBm[5]);
+  const int q = lo_int(t);
+  const double kd = t - kBm[5];
+  double r = fma(-kd, kBm[3], th);
+  r = fma(-kd, kBm[4], r);
+  const double z = r * r;
+  const double v = z * r;
+  const double ps = fma(z, fma(z, fma(z, fma(z, kS[5], kS[4]), kS[3]), kS[2]), kS[1]);
+  const double s = fma(v, fma(z, ps, kS[0]), r);
+  const double pc = z * fma(z, fma(z, fma(z, fma(z, fma(z, kC[5], kC[4]), kC[3]), kC[2]), kC[1]),
+                            kC[0]);
+  const double hz = 0.5 * z;
+  const double w = 1.0 - hz;
+  const double c = w + fma(z, pc, (1.0 - w) - hz);
+  const int swap = q & 1;
+  const double s0 = swap ? c : s, c0 = swap ? s : c;
+  *sn = (q & 2) ? -s0 : s0;
+  *cs = ((q + 1) & 2) ? -c0 : c0;
+}
+
+/* exp(x), expm1(x) for x = -lam h (device ou_exp; libm below -700) */
+static void dm_expm1_exp(double x, double* em1, double* ex) {
+  if (!(x >= -700.0)) {
+    *em1 = expm1(x);
+    *ex = exp(x);
+    return;
+  }
+  const double t = fma(x, kER[0], kER[3]);
+  const int k = lo_int(t);
+  const double kd = t - kER[3];
+  double r = fma(-kd, kER[1], x);
+  r = fma(-kd, kER[2], r);
+  double q = kEP[11];
+  for (int i = 10; i >= 0; --i) q = fma(q, r, kEP[i]);
+  const double P = fma(r * r, q, r);
+  const double s = bitsd((uint64_t)(uint32_t)((k + 1023) << 20) << 32);
+  *em1 = fma(s, P, s - 1.0);
+  *ex = fma(s, P, s);
+}
+
+/* exp(-lam h) (integrators.hpp:31-33), either math */
+static double orc_exp_neg(double lam, double h) {
+  if (!g_devmath) return exp(-lam * h);
+  double em1, ex;
+  dm_expm1_exp(-lam * h, &em1, &ex);
+  return ex;
+}
+
 /* noise.hpp:60-75 — Box-Muller pair of block k>>1; cos for even k, sin for odd. */
 double orc_normal_at(uint64_t seed, uint32_t level, uint64_t idx, uint64_t k) {
   uint32_t key[2];
@@ -67,8 +171,13 @@ double orc_normal_at(uint64_t seed, uint32_t level, uint64_t idx, uint64_t k) {
   orc_philox4x32(ctr, key, w);
   const double u1 = orc_bits_to_unit(w[0], w[1]);
   const double u2 = orc_bits_to_unit(w[2], w[3]);
-  const double r = sqrt(-2.0 * log(u1));
+  const double r = sqrt(-2.0 * (g_devmath ? dm_log_unit(u1) : log(u1)));
   const double th = 2.0 * ORC_PI * u2;
+  if (g_devmath) {
+    double sn, cs;
+    dm_sincos_2pi(th, &sn, &cs);
+    return (k & 1) ? r * sn : r * cs;
+  }
   return (k & 1) ? r * sin(th) : r * cos(th);
 }
 
@@ -80,7 +189,7 @@ double orc_coarse_noise_se(double xi0, double xi1, int s0, int s1, int sc) {
 /* noise.hpp:100-104 */
 double orc_coarse_noise_gl(double xi0, double xi1, double lam, double h, int s0, int s1,
                            int sc) {
-  const double e = exp(-lam * h);
+  const double e = orc_exp_neg(lam, h);
   return sc * (e * (s0 * xi0) + s1 * xi1) / sqrt(e * e + 1.0);
 }
 
@@ -181,8 +290,15 @@ int orc_reflect(double* x, double* u, double H, int* parity, int64_t* n_refl, in
 }
 
 /* integrators.hpp:31-37 */
-static double ou_decay(double lam, double h) { return exp(-lam * h); }
-static double ou_noise_sd(double lam, double h) { return sqrt(-expm1(-2.0 * lam * h) / (2.0 * lam)); }
+static double ou_decay(double lam, double h) { return orc_exp_neg(lam, h); }
+static double ou_noise_sd(double lam, double h) {
+  if (g_devmath) { /* device ou_terms: expm1(2x) = em1 (em1 + 2), x = -lam h */
+    double em1, ex;
+    dm_expm1_exp(-lam * h, &em1, &ex);
+    return sqrt(-(em1 * (em1 + 2.0)) / (2.0 * lam));
+  }
+  return sqrt(-expm1(-2.0 * lam * h) / (2.0 * lam));
+}
 
 /* integrators.hpp:41-43 */
 double orc_se_stability_limit(const ablmc_model_params* p) {
@@ -339,7 +455,7 @@ static double increment_gl(const double* xi, const double* dt, const double* lam
   for (int r = n; r-- > 0;) {
     const double s = is_coarse ? (double)sg[r] : 1.0;
     acc += s * xi[r] * ou_noise_sd(lam[r], dt[r]) * damp;
-    damp *= exp(-lam[r] * dt[r]);
+    damp *= orc_exp_neg(lam[r], dt[r]);
   }
   return (is_coarse ? sc : 1) * acc;
 }

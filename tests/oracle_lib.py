@@ -76,6 +76,7 @@ def orc() -> C.CDLL:
                                                      C.c_double, C.c_uint64, C.c_uint32,
                                                      C.c_uint64, P(C.c_double), P(OrcState),
                                                      P(C.c_int64)]),
+            "orc_set_device_math": (None, [C.c_int]),
             "orc_set_profile": (None, [C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
                                        C.c_double]),
             "orc_build_smoothing_polynomial": (C.c_int, [C.c_int, P(C.c_double)]),

@@ -474,3 +474,66 @@ def test_full_size_c5_properties():
     ratio = one.variance() / l9.variance()
     assert 0.2 < ratio < 0.55, ratio
     assert abs(one.mean()) < 6 * one.std_error() + 1e-4  # E[Y_10] ~ c h: tiny
+
+
+# ------------------------------------------ device elementary functions
+# The only arithmetic not taken from the reference is the elementary
+# functions (Box-Muller log/sin/cos, the OU exp/expm1), restated from fdlibm /
+# Cody-Waite within 1-2 ulp of glibc.  With the oracle switched to the
+# device's own restatement of them (orc_set_device_math) every integrator's
+# path must be bit-identical: everything else is the reference's arithmetic.
+def _params_of(d):
+    return O.default_params(**{k: d[k] for k in ("kappa_sigma", "kappa_tau", "u_star", "H",
+                                                   "eps_reg", "x_ref", "noise_scale")})
+
+
+@pytest.fixture
+def device_math():
+    O.orc().orc_set_device_math(1)
+    yield
+    O.orc().orc_set_device_math(0)
+
+
+@pytest.mark.parametrize("case_idx", range(16))
+def test_pairs_bit_exact_given_device_math(ref_vectors, case_idx, device_math):
+    case = ref_vectors["pairs"][case_idx]
+    d = case["problem"]
+    pr = make_problem(d)
+    level, first = case["level"], case["first"]
+    count = len(case["states"])
+    M = d["m0"] << level
+    p = _params_of(d)
+    xi = stream_xi(d["seed"], level, first, count, M)  # glibc normals, host-supplied
+    for mode, x in (("oracle", xi), ("philox", None)):
+        got = ablmc.simulate_pairs(pr, level, first, count, xi=x)
+        for i in range(count):
+            rc, f, c = O.orc_pair(d["integrator"], p, d["x0"], d["u0"], d["T"], M, d["seed"],
+                                  level, first + i, xi=None if x is None else x[i],
+                                  signs_on=d["signs_on"])
+            g = got[i]
+            assert (rc == 0) == bool(g["fok"]), (case["name"], mode, i)
+            if rc == 0:
+                assert ([g["fx"], g["fu"], g["fpar"], g["fn"], g["cx"], g["cu"], g["cpar"], g["cn"]]
+                        == [f.x, f.u, f.parity, f.n_refl, c.x, c.u, c.parity, c.n_refl]), (
+                    case["name"], mode, i)
+
+
+@pytest.mark.parametrize("ig", list(Ig))
+def test_paths_and_sums_bit_exact_given_device_math(ig, device_math):
+    pr = ablmc.Problem.make(ablmc.ModelParams(), ig, ablmc.QoISpec(kind=ablmc.QoIKind.smoothed_indicator),
+                            0.05, 0.1, 1.0, 40, 77)
+    got = ablmc.simulate_paths(pr, 40, 0, 256, 0)
+    p = O.default_params()
+    for i in range(256):
+        rc, s = O.orc_path(int(ig), p, 0.05, 0.1, 1.0, 40, 77, 0, i)
+        assert rc == 0 and [got["x"][i], got["u"][i], got["parity"][i], got["n_refl"][i]] == [
+            s.x, s.u, s.parity, s.n_refl], i
+    for level in (0, 3):
+        acc = ablmc.LevelStats().init(level, pr.h_level(level), 1)
+        ablmc.accumulate_samples(acc, 11, 9000, pr, level)
+        st = O.Stats(1)
+        assert O.orc().orc_accumulate_samples(C.byref(pr._c), level, 11, 9000, C.byref(st.c)) == 0
+        assert (acc.n, acc.failed, acc.cost_steps) == (st.n, st.failed, st.cost_steps)
+        # same samples bit for bit; only the summation tree differs
+        assert close(acc.sum_y, st.sum_y, 1e-13, 1e-15)
+        assert close(acc.sum_y2, st.sum_y2, 1e-13, 1e-15)
