@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstddef>
 
 #include "level_common.cuh"
 
@@ -98,9 +99,40 @@ struct ALeg {
   PState s;
   Coef c;         // sde_coeffs(s.x)
   double t, t_next, h_cur;
-  double acc;     // SE: sum S_j xi_j sqrt(dtau_j); GL: Horner form of the OU-weighted sum
+  double acc;     // SE: sum S_j xi_j sqrt(dtau_j); GL/BAOAB: Horner form of the OU-weighted
+                  // sum (used only when more sub-intervals are pending than are stored)
   long long steps;
+  int np;         // GL/BAOAB: pending sub-intervals of the current step
   bool done;
+};
+
+// GL/BAOAB pending terms (timeline.hpp:86-105): term_r = S_r xi_r sd(lam, dt_r)
+// and e_r = exp(-lam dt_r) of each pending sub-interval, so the increment is
+// the reference's backward sum acc += term_r damp, damp *= e_r (r = n-1..0),
+// bit for bit.  The persistent kernel keeps the first kPend of them per leg
+// in shared memory and the next kPendLocal - kPend in local memory (a coarse
+// step near the ground can span many fine sub-intervals); the
+// one-thread-per-sample kernels keep kPendLocal in local memory.  Beyond
+// kPendLocal the Horner form (equal for <= 2 terms, within rounding beyond)
+// is used (the persistent FAST kernel hands such samples to K1R first).
+constexpr int kPend = 8;
+constexpr int kPendLocal = 64;
+struct PendSpill {  // persistent kernel: pending terms kPend .. kPendLocal-1, per leg
+  double t[2][kPendLocal - kPend], e[2][kPendLocal - kPend];
+};
+
+template <class Term, class Decay>
+__device__ __forceinline__ double backward_sum(int n, Term term, Decay decay) {
+  double acc = 0.0, damp = 1.0;
+  for (int r = n - 1; r >= 0; --r) {
+    acc = add(acc, mul(term(r), damp));
+    damp = mul(damp, decay(r));
+  }
+  return acc;
+}
+
+struct PendLocal {
+  double t[kPendLocal], e[kPendLocal];
 };
 
 // coupling.hpp:140-155
@@ -119,19 +151,32 @@ __device__ __forceinline__ void leg_schedule(ALeg& L, double base, double T, dou
 
 // Pending sub-interval (tau, tau + dt) with draw xi and coupling sign S
 // (timeline.hpp:75-105 terms).  SE: S xi sqrt(dt), summed forward as the
-// reference does.  GL: sum_r S_r xi_r sd(lam, dt_r) prod_{q > r} exp(-lam dt_q)
-// in Horner form acc <- acc e_r + term_r: the reference's backward sum for
-// up to two pending sub-intervals, within rounding beyond.
+// reference does.  GL/BAOAB: the term S xi sd(lam, dt) and weight
+// exp(-lam dt) are stored for the backward sum at the step (leg_settle);
+// the Horner form acc <- acc e + term is kept alongside for overflow.
 template <int IG, int FAST>
-__device__ __forceinline__ void leg_push(ALeg& L, double xi_s, double dt, double sqrt_dt,
-                                         bool& bad) {
+__device__ __forceinline__ void leg_push(ALeg& L, PendLocal& P, double xi_s, double dt,
+                                         double sqrt_dt, bool& bad) {
   if (IG == kSE) {
     L.acc = add(L.acc, mul(xi_s, sqrt_dt));
   } else {
     double e, sd;
     ou_terms<FAST>(L.c.lam, dt, e, sd, bad);
-    L.acc = add(mul(L.acc, e), mul(xi_s, sd));
+    const double term = mul(xi_s, sd);
+    if (L.np < kPendLocal) {
+      P.t[L.np] = term;
+      P.e[L.np] = e;
+    }
+    ++L.np;
+    L.acc = add(mul(L.acc, e), term);
   }
+}
+
+// the pending increment of a GL/BAOAB leg about to step (register version)
+template <int IG>
+__device__ __forceinline__ void leg_settle(ALeg& L, const PendLocal& P) {
+  if (IG != kSE && L.np <= kPendLocal)
+    L.acc = backward_sum(L.np, [&](int r) { return P.t[r]; }, [&](int r) { return P.e[r]; });
 }
 
 // coupling.hpp:158-173 — the leg's step with the equivalent normal of its
@@ -160,6 +205,7 @@ __device__ __forceinline__ bool leg_take(ALeg& L, bool is_coarse, const DevModel
   L.t = L.t_next;
   ++L.steps;
   L.acc = 0.0;
+  L.np = 0;
   return ok;
 }
 
@@ -177,11 +223,13 @@ __device__ __forceinline__ PathOut run_pair_adaptive(const KernelArgs& a, uint64
   f.t = 0.0;
   f.acc = 0.0;
   f.steps = 0;
+  f.np = 0;
   f.done = false;
   ALeg c = f;
   leg_schedule<FAST>(f, hb, T, lam_ref, bad);
   leg_schedule<FAST>(c, hb2, T, lam_ref, bad);
   SeqNoise<PhiloxKey> ns;
+  PendLocal pf, pc;
   const bool signs = a.signs_on;
   PathOut o;
   o.ok = true;
@@ -195,15 +243,17 @@ __device__ __forceinline__ PathOut run_pair_adaptive(const KernelArgs& a, uint64
       const double xi = ns.next(idx, a.key);
       const double sqrt_dt = IG == kSE ? O::sqrt(dt, bad) : 0.0;
       const int sf = signs ? f.s.par : 1;
-      if (!f.done) leg_push<IG, FAST>(f, xi, dt, sqrt_dt, bad);
-      if (!c.done) leg_push<IG, FAST>(c, sgn(sf, xi), dt, sqrt_dt, bad);
+      if (!f.done) leg_push<IG, FAST>(f, pf, xi, dt, sqrt_dt, bad);
+      if (!c.done) leg_push<IG, FAST>(c, pc, sgn(sf, xi), dt, sqrt_dt, bad);
     }
     if (!f.done && f.t_next == tau) {
+      leg_settle<IG>(f, pf);
       if (!leg_take<IG, PROF, FAST>(f, false, m, bad)) { o.ok = false; break; }
       if (f.t_next >= T) f.done = true;
       else leg_schedule<FAST>(f, hb, T, lam_ref, bad);
     }
     if (!c.done && c.t_next == tau) {
+      leg_settle<IG>(c, pc);
       if (!leg_take<IG, PROF, FAST>(c, true, m, bad)) { o.ok = false; break; }
       if (c.t_next >= T) c.done = true;
       else leg_schedule<FAST>(c, hb2, T, lam_ref, bad);
@@ -284,7 +334,7 @@ __device__ __forceinline__ void adaptive_store(const KernelArgs& a, int64_t j, c
 // two consecutive events, in the same order, without a draw).
 struct LegHot {
   double t_next, acc, lam;
-  int par;
+  int par, np;
   bool done;
 };
 enum { kColdX, kColdU, kColdSu2, kColdSig, kColdDsu2, kColdRsu2, kColdT, kColdH, kColdN };
@@ -292,7 +342,12 @@ struct LegStore {
   double d[kColdN][2][kTile];
   long long steps[2][kTile];
   int nrefl[2][kTile];
+  double pt[kPend][2][kTile], pe[kPend][2][kTile];  // GL/BAOAB only (SE launches without)
 };
+template <int IG>
+constexpr size_t leg_store_bytes() {
+  return IG == kSE ? offsetof(LegStore, pt) : sizeof(LegStore);
+}
 
 struct PairSM {
   LegHot f, c;
@@ -303,7 +358,7 @@ struct PairSM {
 };
 
 __device__ __forceinline__ LegHot leg_hot(const ALeg& L) {
-  return {L.t_next, L.acc, L.c.lam, L.s.par, L.done};
+  return {L.t_next, L.acc, L.c.lam, L.s.par, L.np, L.done};
 }
 
 __device__ __forceinline__ void leg_store(LegStore& st, int leg, const ALeg& L) {
@@ -334,28 +389,42 @@ __device__ __forceinline__ ALeg leg_load(const LegStore& st, int leg, const LegH
   L.h_cur = st.d[kColdH][leg][i];
   L.acc = h.acc;
   L.steps = st.steps[leg][i];
+  L.np = h.np;
   L.done = h.done;
   return L;
 }
 
-// pending-increment update on the hot fields (leg_push on LegHot)
+// pending-increment update on the hot fields (leg_push on LegHot); GL/BAOAB
+// terms go to shared memory (overflow: FAST recomputes the sample in K1R)
 template <int IG, int FAST>
-__device__ __forceinline__ void hot_push(LegHot& L, double xi_s, double dt, double sqrt_dt,
-                                         bool& bad) {
+__device__ __forceinline__ void hot_push(LegHot& L, LegStore& st, PendSpill& sp, int leg,
+                                         double xi_s, double dt, double sqrt_dt, bool& bad) {
   if (IG == kSE) {
     L.acc = add(L.acc, mul(xi_s, sqrt_dt));
   } else {
     double e, sd;
     ou_terms<FAST>(L.lam, dt, e, sd, bad);
-    L.acc = add(mul(L.acc, e), mul(xi_s, sd));
+    const double term = mul(xi_s, sd);
+    if (L.np < kPend) {
+      st.pt[L.np][leg][threadIdx.x] = term;
+      st.pe[L.np][leg][threadIdx.x] = e;
+    } else if (L.np < kPendLocal) {
+      sp.t[leg][L.np - kPend] = term;
+      sp.e[leg][L.np - kPend] = e;
+    } else if (FAST) {
+      bad = true;
+    }
+    ++L.np;
+    L.acc = add(mul(L.acc, e), term);
   }
 }
 
 // One event of simulate_pair_adaptive (coupling.hpp:175-211).  Returns true
 // when the sample is finished (both legs at T, or failed).
 template <int IG, int PROF, int FAST>
-__device__ __forceinline__ bool pair_event(PairSM& S, LegStore& st, const KernelArgs& a,
-                                           uint64_t idx, double lam_ref, bool& ok, bool& bad) {
+__device__ __forceinline__ bool pair_event(PairSM& S, LegStore& st, PendSpill& sp,
+                                           const KernelArgs& a, uint64_t idx, double lam_ref,
+                                           bool& ok, bool& bad) {
   using O = Ops<FAST>;
   const double T = a.T;
   bool take_fine;
@@ -367,8 +436,8 @@ __device__ __forceinline__ bool pair_event(PairSM& S, LegStore& st, const Kernel
       const double xi = S.ns.next(idx, a.key);
       const double sqrt_dt = IG == kSE ? O::sqrt(dt, bad) : 0.0;
       const int sf = a.signs_on ? S.f.par : 1;
-      if (!S.f.done) hot_push<IG, FAST>(S.f, xi, dt, sqrt_dt, bad);
-      if (!S.c.done) hot_push<IG, FAST>(S.c, sgn(sf, xi), dt, sqrt_dt, bad);
+      if (!S.f.done) hot_push<IG, FAST>(S.f, st, sp, 0, xi, dt, sqrt_dt, bad);
+      if (!S.c.done) hot_push<IG, FAST>(S.c, st, sp, 1, sgn(sf, xi), dt, sqrt_dt, bad);
     }
     take_fine = !S.f.done && S.f.t_next == S.tau;
     S.pend_c = take_fine && !S.c.done && S.c.t_next == S.tau;
@@ -378,6 +447,12 @@ __device__ __forceinline__ bool pair_event(PairSM& S, LegStore& st, const Kernel
   }
   const int leg = take_fine ? 0 : 1;
   ALeg W = leg_load(st, leg, take_fine ? S.f : S.c);
+  if (IG != kSE && W.np <= kPendLocal) {
+    const int i = threadIdx.x;
+    W.acc = backward_sum(
+        W.np, [&](int r) { return r < kPend ? st.pt[r][leg][i] : sp.t[leg][r - kPend]; },
+        [&](int r) { return r < kPend ? st.pe[r][leg][i] : sp.e[leg][r - kPend]; });
+  }
   ok = leg_take<IG, PROF, FAST>(W, !take_fine, a.model, bad);
   if (W.t_next >= T) W.done = true;
   else leg_schedule<FAST>(W, take_fine ? a.h_base : mul(2.0, a.h_base), T, lam_ref, bad);
@@ -442,6 +517,7 @@ __global__ void __launch_bounds__(kTile, ABLMC_MINB_ADAPTIVE) k_adaptive_persist
   f0.t = 0.0;
   f0.acc = 0.0;
   f0.steps = 0;
+  f0.np = 0;
   f0.done = false;
   ALeg c0 = f0;
   if (COUPLED) {
@@ -452,6 +528,7 @@ __global__ void __launch_bounds__(kTile, ABLMC_MINB_ADAPTIVE) k_adaptive_persist
   extern __shared__ double4 ad_smem[];
   LegStore& st = *reinterpret_cast<LegStore*>(ad_smem);  // COUPLED only (dynamic size 0 else)
   PairSM P;
+  PendSpill sp;
   PathSM Q;
   auto start = [&]() {
     if (COUPLED) {
@@ -477,7 +554,7 @@ __global__ void __launch_bounds__(kTile, ABLMC_MINB_ADAPTIVE) k_adaptive_persist
   while (j < a.n) {
     const uint64_t idx = uint64_t(a.first + a.offset + j);
     bool ok = true;
-    const bool fin = COUPLED ? pair_event<IG, PROF, FAST>(P, st, a, idx, lam_ref, ok, bad)
+    const bool fin = COUPLED ? pair_event<IG, PROF, FAST>(P, st, sp, a, idx, lam_ref, ok, bad)
                              : path_event<IG, PROF, FAST>(Q, a, idx, lam_ref, ok, bad);
     if (fin) {
       if (FAST && bad) {
@@ -542,8 +619,10 @@ cudaError_t launch_adaptive(const KernelArgs& a, double* tile_sums, long long* t
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t tiles = (a.n + kTile - 1) / kTile;
   const bool fast = a.fast != 0;
-  const size_t smem = COUPLED ? sizeof(LegStore) : 0;
+  const size_t smem = COUPLED ? leg_store_bytes<IG>() : 0;
   auto run = [&](auto kernel) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kTile, smem);
     const unsigned grid = unsigned(std::min<int64_t>(tiles, int64_t(sms) * std::max(per_sm, 1)));
     kernel<<<grid, kTile, smem, st>>>(a);

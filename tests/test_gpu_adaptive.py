@@ -12,13 +12,13 @@ the DEVICE's own normal stream (ablmc_normals: the kernel's Philox words and
 Box-Muller), and
 * SE: bit-identical states, parities, reflection counts, ok flags, steps and
   per-level sums (up to summation order) -- exact arithmetic end to end;
-* GL/BAOAB: the OU weights use the device exp/expm1 (<= 1-2 ulp from glibc)
-  and GL's pending weights are summed in Horner form (equal to the
-  reference's backward sum for up to two pending sub-intervals), so states
-  agree within rel 1e-9 except on samples where the reference itself is
-  ulp-sensitive: the fraction of differing samples may not exceed the
-  reference's own sensitivity (oracle with device vs glibc normals) + 5%
-  (+ 2 sigma of that count).
+* GL/BAOAB: the OU weights use the device exp/expm1 (<= 1-2 ulp from glibc),
+  so against the glibc oracle states agree within rel 1e-9 except on samples
+  where the reference itself is ulp-sensitive: the fraction of differing
+  samples may not exceed the reference's own sensitivity (oracle with device
+  vs glibc normals) + 5% (+ 2 sigma of that count); with the oracle on the
+  device's elementary functions too (orc_set_device_math) every integrator
+  is bit-identical (test_adaptive_*_given_device_math).
 Against the reference's own glibc-normal stream the level statistics agree
 within their standard errors (test_adaptive_level_mean_vs_oracle).
 """
@@ -269,3 +269,51 @@ def test_adaptive_golden_accumulate_statistics(ref_vectors):
         n = acc.n
         var = np.maximum(sy2 / n - (sy / n) ** 2, 0.0)
         assert np.all(np.abs(acc.sum_y / n - sy / n) <= 4 * np.sqrt(2 * var / n) + 1e-12), case
+
+
+@pytest.fixture
+def device_math():
+    O.orc().orc_set_device_math(1)
+    yield
+    O.orc().orc_set_device_math(0)
+
+
+@pytest.mark.parametrize("cfg", CONFIGS, ids=lambda c: f"{c['ig'].name}-l{c['level']}")
+def test_adaptive_pairs_bit_exact_given_device_math(cfg, device_math):
+    """With the oracle on the device's own elementary functions
+    (orc_set_device_math) and Philox stream, every integrator's adaptive pair
+    is bit-identical: the GL/BAOAB pending increments are the reference's
+    backward sums (pending terms kept per leg), so the only non-reference
+    arithmetic left is log/sin/cos/exp/expm1."""
+    cfg = dict(cfg)
+    level = cfg.pop("level")
+    pr = problem(seed=31, **cfg)
+    c = pr._c
+    n = 96
+    got = ablmc.simulate_pairs(pr, level, 1000, n)
+    M = c.m0 << level
+    for i in range(n):
+        rc, f, cc, _ = O.orc_pair_adaptive(c.integrator, c.params, c.x0, c.u0, c.T, c.T / M,
+                                           c.x_adapt, c.seed, level, 1000 + i, c.signs_on)
+        g = got[i]
+        assert (rc == 0) == bool(g["fok"]), i
+        if rc == 0:
+            assert ([g["fx"], g["fu"], g["fpar"], g["fn"], g["cx"], g["cu"], g["cpar"], g["cn"]]
+                    == [f.x, f.u, f.parity, f.n_refl, cc.x, cc.u, cc.parity, cc.n_refl]), i
+
+
+@pytest.mark.parametrize("ig", [Ig.se, Ig.gl, Ig.baoab])
+def test_adaptive_accumulate_given_device_math(ig, device_math):
+    """Level sums of the persistent kernel (pending terms in shared memory,
+    overflow recomputed by K1R) against the oracle on the device math: same
+    samples, same steps; only the summation tree differs."""
+    q = ablmc.QoISpec(kind=ablmc.QoIKind.smoothed_indicator)
+    pr = problem(ig, x0=0.02, m0=20, x_adapt=0.3, seed=5, qoi=q)
+    for level in (0, 3):
+        acc = ablmc.LevelStats().init(level, pr.h_level(level), 1)
+        ablmc.accumulate_samples(acc, 3, 4000, pr, level)
+        st = O.Stats(1)
+        assert O.orc().orc_accumulate_samples(C.byref(pr._c), level, 3, 4000, C.byref(st.c)) == 0
+        assert (acc.n, acc.failed, acc.cost_steps) == (st.n, st.failed, st.cost_steps)
+        assert close(acc.sum_y, st.sum_y, 1e-13, 1e-15)
+        assert close(acc.sum_y2, st.sum_y2, 1e-13, 1e-15)
