@@ -115,7 +115,10 @@ struct ALeg {
 // one-thread-per-sample kernels keep kPendLocal in local memory.  Beyond
 // kPendLocal the Horner form (equal for <= 2 terms, within rounding beyond)
 // is used (the persistent FAST kernel hands such samples to K1R first).
-constexpr int kPend = 8;
+#ifndef ABLMC_KPEND
+#define ABLMC_KPEND 8
+#endif
+constexpr int kPend = ABLMC_KPEND;
 constexpr int kPendLocal = 64;
 struct PendSpill {  // persistent kernel: pending terms kPend .. kPendLocal-1, per leg
   double t[2][kPendLocal - kPend], e[2][kPendLocal - kPend];
