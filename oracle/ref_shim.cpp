@@ -192,6 +192,21 @@ int ref_step(int ig, ablmc_path_state* s, double h, double xi, const ablmc_model
   }
 }
 
+// Extended-SDE oracle (integrators.hpp:119-189, acceptance criterion 7): n
+// steps of extended_step_oracle from (x0, u0) with draws xi[0..n), folded back
+// to the physical state (X, U) = S (eta(x~), u~) with S = fold_sign.
+void ref_extended_path(int ig, const ablmc_model_params* m, double x0, double u0, double h,
+                       int64_t n, const double* xi, double out_xu[2], int* out_sign) {
+  const ModelParams p = to_params(*m);
+  ExtendedState e{x0, u0, 0.0};
+  for (int64_t k = 0; k < n; ++k) e = extended_step_oracle(e, h, xi[k], p, to_ig(ig));
+  const double eta = fold_height(e.x, p.H);
+  const int sign = eta >= 0.0 ? +1 : -1;
+  out_xu[0] = sign * eta;
+  out_xu[1] = sign * e.u;
+  *out_sign = sign;
+}
+
 // simulate_pair on NoiseStream(seed, level, idx) for idx in [first, first+count).
 void ref_pair_states(const ablmc_problem* pr, int level, int64_t first, int64_t count,
                      ablmc_pair_state* out) {

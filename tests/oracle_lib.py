@@ -117,6 +117,9 @@ def ref() -> C.CDLL | None:
                                       P(C.c_double), P(C.c_int), P(C.c_int64)]),
             "ref_step": (C.c_int, [C.c_int, P(capi.PathStateC), C.c_double, C.c_double,
                                    P(capi.ModelParamsC), C.c_int, P(C.c_int)]),
+            "ref_extended_path": (None, [C.c_int, P(capi.ModelParamsC), C.c_double, C.c_double,
+                                         C.c_double, C.c_int64, P(C.c_double), P(C.c_double),
+                                         P(C.c_int)]),
             "ref_pair_states": (None, [P(capi.ProblemC), C.c_int, C.c_int64, C.c_int64,
                                        P(capi.PairStateC)]),
             "ref_path_states": (None, [P(capi.ProblemC), C.c_int64, C.c_uint32, C.c_int64,
