@@ -507,6 +507,13 @@ def allocate_samples(var: Sequence[float], h: Sequence[float], eps: float) -> li
     return list(out)
 
 
+def build_smoothing_polynomial(r: int) -> list[float]:
+    """qoi.hpp:31-77: coefficients of g_r (r + 2 of them)."""
+    out = (C.c_double * 16)()
+    _check(lib().ablmc_build_smoothing_polynomial(int(r), out))
+    return list(out)[: int(r) + 2]
+
+
 def adaptive_step_size(x: float, h: float, x_adapt: float, params: ModelParams) -> float:
     """timeline.hpp:18-23."""
     p = params.c()

@@ -165,6 +165,7 @@ SIGNATURES = {
                                       C.c_int, P(C.c_int)]),
     "ablmc_allocate_samples": (C.c_int, [P(C.c_double), P(C.c_double), C.c_int, C.c_double,
                                          P(C.c_int64)]),
+    "ablmc_build_smoothing_polynomial": (C.c_int, [C.c_int, P(C.c_double)]),
     "ablmc_adaptive_step_size": (C.c_double, [C.c_double, C.c_double, C.c_double,
                                               P(ModelParamsC)]),
     "ablmc_run_config_defaults": (None, [P(RunConfigC)]),

@@ -254,3 +254,30 @@ def test_adaptive_step_size_goldens():
     assert ablmc.adaptive_step_size(0.05, 0.025, 0.05, mp) == 0.025
     v = ablmc.adaptive_step_size(0.01, 0.025, 0.05, mp)
     assert abs(v - 0.19390825748466839 * 0.025) <= 1e-12 * 0.19390825748466839 * 0.025
+
+
+def test_smoothing_polynomial_product_vs_goldens_and_criterion_9():
+    """The product's host polynomial (used by the device QoI): the
+    reference's golden coefficients (test_qoi.cpp:33-59) bit for bit vs the
+    pinned oracle, and acceptance criterion 9 (acceptance.cpp:367-391): r = 2
+    coefficients (1/2, -9/8, 0, 5/8) to 1e-12, g(-1) = 1, g(1) = 0 and the
+    moment conditions to 1e-10 for r <= 8."""
+    import oracle_lib as O
+    for r in range(0, 13):
+        got = ablmc.build_smoothing_polynomial(r)
+        c = (C.c_double * (r + 2))()
+        assert O.orc().orc_build_smoothing_polynomial(r, c) == 0
+        assert got == list(c), r
+    p2 = ablmc.build_smoothing_polynomial(2)
+    assert max(abs(a - b) for a, b in zip(p2, [0.5, -1.125, 0.0, 0.625])) <= 1e-12
+    worst = 0.0
+    for r in range(0, 9):
+        p = ablmc.build_smoothing_polynomial(r)
+        ev = lambda s: sum(ci * s ** i for i, ci in enumerate(p))  # noqa: E731
+        worst = max(worst, abs(ev(-1.0) - 1.0), abs(ev(1.0)))
+        for j in range(r):
+            m = sum(p[i] * 2.0 / (i + j + 1) for i in range(len(p)) if (i + j) % 2 == 0)
+            worst = max(worst, abs(m - (1.0 if j % 2 == 0 else -1.0) / (j + 1)))
+    assert worst <= 1e-10
+    with pytest.raises(ValueError, match="r must be"):
+        ablmc.build_smoothing_polynomial(13)
