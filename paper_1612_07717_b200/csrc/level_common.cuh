@@ -91,13 +91,16 @@ __device__ __forceinline__ PathOut run_sample(const KernelArgs& a, uint64_t idx,
     }
     bool ok;
     if (IG == kSE) {
+      // the coarse coefficients do not depend on the fine steps: issued first
+      // so the scheduler can interleave the two chains
+      const Coef ccw = coeffs<PROF, FAST>(o.c.x, m, bad);
       const int p0 = o.f.par;
       ok = se_step<PROF, FAST>(o.f, h, sqrt_h, xi0, m, bad);
       const int p1 = o.f.par;
       ok = ok && se_step<PROF, FAST>(o.f, h, sqrt_h, xi1, m, bad);
       const int s0 = signs ? p0 : 1, s1 = signs ? p1 : 1, sc = signs ? o.c.par : 1;
-      ok = ok && se_step<PROF, FAST>(o.c, h2, sqrt_h2,
-                                     coarse_noise_se<FAST>(xi0, xi1, s0, s1, sc, bad), m, bad);
+      ok = ok && se_update<FAST>(o.c, ccw, h2, sqrt_h2,
+                                 coarse_noise_se<FAST>(xi0, xi1, s0, s1, sc, bad), m, bad);
     } else if (IG == kGL) {
       const int p0 = o.f.par;
       double e0, e1, ec;
