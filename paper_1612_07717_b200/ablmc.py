@@ -274,6 +274,20 @@ def accumulate_samples(acc: LevelStats, first: int, count: int, pr: Problem, lev
     acc._take(v)
 
 
+def accumulate_levels(requests: Sequence[tuple], pr: Problem) -> None:
+    """Several accumulate_samples calls in one device batch: requests are
+    (acc, first, count, level) tuples; each acc ends as after its own call."""
+    n = len(requests)
+    views = [r[0]._view() for r in requests]
+    lv = (C.c_int * n)(*[int(r[3]) for r in requests])
+    fs = (C.c_int64 * n)(*[int(r[1]) for r in requests])
+    cs = (C.c_int64 * n)(*[int(r[2]) for r in requests])
+    ptrs = (C.POINTER(capi.LevelStatsC) * n)(*[_P(v) for v in views])
+    _check(lib().ablmc_accumulate_levels(_P(pr._c), n, lv, fs, cs, ptrs))
+    for r, v in zip(requests, views):
+        r[0]._take(v)
+
+
 def accumulate_paths(acc: LevelStats, first: int, count: int, pr: Problem, M: int,
                      stream_level: int = 0) -> None:
     """Device replacement for ``accumulate_samples(..., pr.path_sampler(M, stream_level))``."""

@@ -127,6 +127,8 @@ SIGNATURES = {
     "ablmc_check_failure_budget": (C.c_int, [P(LevelStatsC)]),
     "ablmc_accumulate_samples": (C.c_int, [P(ProblemC), C.c_int, C.c_int64, C.c_int64,
                                            P(LevelStatsC)]),
+    "ablmc_accumulate_levels": (C.c_int, [P(ProblemC), C.c_int, P(C.c_int), P(C.c_int64),
+                                          P(C.c_int64), P(P(LevelStatsC))]),
     "ablmc_accumulate_paths": (C.c_int, [P(ProblemC), C.c_int64, C.c_uint32, C.c_int64,
                                          C.c_int64, P(LevelStatsC)]),
     "ablmc_num_superblocks": (C.c_int64, [C.c_int64]),

@@ -81,6 +81,39 @@ int accumulate_level(const ablmc_problem* pr, Stats& st, int level, int64_t firs
   return ablmc_check_failure_budget(&v);
 }
 
+// Several levels at once: `ensure_level(l, n_target)` for each (level,
+// target) in order, as one device batch (ablmc_accumulate_levels: one
+// synchronisation, same bits as the sequential calls); failure budgets are
+// checked afterwards in the same order.
+int accumulate_levels(const ablmc_problem* pr, std::vector<Stats>& levels,
+                      const std::vector<std::pair<int, int64_t>>& want) {
+  std::vector<int> ls;
+  std::vector<int64_t> firsts, counts;
+  std::vector<ablmc_level_stats> views;
+  std::vector<size_t> idx;
+  views.reserve(want.size());
+  for (const auto& w : want) {
+    Stats& st = levels[size_t(w.first)];
+    if (st.n >= w.second) continue;
+    ls.push_back(w.first);
+    firsts.push_back(st.attempts());
+    counts.push_back(w.second - st.n);
+    views.push_back(st.view());
+    idx.push_back(size_t(w.first));
+  }
+  if (ls.empty()) return 0;
+  std::vector<ablmc_level_stats*> ptrs;
+  for (auto& v : views) ptrs.push_back(&v);
+  if (int rc = ablmc_accumulate_levels(pr, int(ls.size()), ls.data(), firsts.data(),
+                                       counts.data(), ptrs.data()))
+    return rc;
+  for (size_t q = 0; q < ls.size(); ++q) {
+    levels[idx[q]].take(views[q]);
+    if (int rc = ablmc_check_failure_budget(&views[q])) return rc;
+  }
+  return 0;
+}
+
 int accumulate_path(const ablmc_problem* pr, Stats& st, int64_t M, int64_t first, int64_t count) {
   ablmc_level_stats v = st.view();
   if (int rc = ablmc_accumulate_paths(pr, M, 0, first, count, &v)) return rc;
@@ -306,11 +339,27 @@ int ablmc_run_mlmc(const ablmc_problem* pr, double eps, const ablmc_mlmc_options
     return pts;
   };
 
+  // the levels vector grown to hold level `l` (ensure_level's first half)
+  auto have_level = [&](int l) {
+    while (int(levels.size()) <= l) {
+      Stats st;
+      const int nl = int(levels.size());
+      st.init(nl, pr->T / double(pr->m0 << nl), dim);
+      levels.push_back(std::move(st));
+    }
+  };
+  // ensure_level over several levels, as one device batch
+  auto ensure_levels = [&](const std::vector<std::pair<int, int64_t>>& want) -> int {
+    for (const auto& w : want) have_level(w.first);
+    return accumulate_levels(pr, levels, want);
+  };
+
   auto fit_with_refinement = [&](int up_to, BiasFit& fit) -> int {
     int64_t n = o.pilot_n;
     for (int attempt = 0;; ++attempt) {
-      for (int l = 1; l <= up_to; ++l)
-        if (int rc = ensure_level(l, n)) return rc;
+      std::vector<std::pair<int, int64_t>> want;
+      for (int l = 1; l <= up_to; ++l) want.push_back({l, n});
+      if (int rc = ensure_levels(want)) return rc;
       const int rc = estimate_bias_constants(bias_points(up_to), fit);
       if (rc == 0) return 0;
       if (rc != ABLMC_ERR_RUNTIME || attempt >= 6) return rc;  // catch (runtime_error)
@@ -333,8 +382,11 @@ int ablmc_run_mlmc(const ablmc_problem* pr, double eps, const ablmc_mlmc_options
       if (int rc = choose_levels(fit.alpha, fit.c1, eps, pr->m0, pr->T, o.l_max, L)) return rc;
     }
   }
-  for (int l = 0; l <= L; ++l)
-    if (int rc = ensure_level(l, o.init_n)) return rc;
+  {
+    std::vector<std::pair<int, int64_t>> want;
+    for (int l = 0; l <= L; ++l) want.push_back({l, o.init_n});
+    if (int rc = ensure_levels(want)) return rc;
+  }
   for (const auto& st : levels) out->pilot_cost_steps += st.cost_steps;
 
   int n_warn = 0, warn_mask = 0;
@@ -350,9 +402,10 @@ int ablmc_run_mlmc(const ablmc_problem* pr, double eps, const ablmc_mlmc_options
       hs[size_t(l)] = levels[size_t(l)].h;
     }
     const std::vector<int64_t> target = allocate_samples(v, hs, eps);
+    std::vector<std::pair<int, int64_t>> want;
     for (int l = 0; l <= L; ++l)
-      if (target[size_t(l)] > levels[size_t(l)].n)
-        if (int rc = ensure_level(l, target[size_t(l)])) return rc;
+      if (target[size_t(l)] > levels[size_t(l)].n) want.push_back({l, target[size_t(l)]});
+    if (int rc = ensure_levels(want)) return rc;
     double stat2 = 0.0;
     for (int l = 0; l <= L; ++l)
       stat2 += levels[size_t(l)].max_variance() / double(levels[size_t(l)].n);
@@ -485,10 +538,19 @@ int ablmc_decay_sweep(const ablmc_problem* pr, int l_min, int l_max, int64_t n_p
   if (int rc = ablmc_host::validate(pr)) return rc;
   if (int rc = ablmc_check_se_stability(pr, pr->T / double(pr->m0))) return rc;
   const int64_t dim = ablmc_host::dim_of(pr);
+  if (l_min < 0 || l_max < l_min) {
+    set_error("decay_sweep: need 0 <= l_min <= l_max");
+    return ABLMC_ERR_INVALID_ARGUMENT;
+  }
+  std::vector<Stats> levels(size_t(l_max) + 1);
+  std::vector<std::pair<int, int64_t>> want;
   for (int l = l_min; l <= l_max; ++l) {
-    Stats st;
-    st.init(l, pr->T / double(pr->m0 << l), dim);
-    if (int rc = accumulate_level(pr, st, l, 0, n_per_level)) return rc;
+    levels[size_t(l)].init(l, pr->T / double(pr->m0 << l), dim);
+    want.push_back({l, n_per_level});
+  }
+  if (int rc = accumulate_levels(pr, levels, want)) return rc;  // one device batch
+  for (int l = l_min; l <= l_max; ++l) {
+    const Stats& st = levels[size_t(l)];
     size_t imax = 0;
     for (size_t i = 1; i < size_t(dim); ++i)
       if (st.variance(i) > st.variance(imax)) imax = i;

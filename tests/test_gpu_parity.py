@@ -537,3 +537,24 @@ def test_paths_and_sums_bit_exact_given_device_math(ig, device_math):
         # same samples bit for bit; only the summation tree differs
         assert close(acc.sum_y, st.sum_y, 1e-13, 1e-15)
         assert close(acc.sum_y2, st.sum_y2, 1e-13, 1e-15)
+
+
+def test_accumulate_levels_batch_equals_sequential_calls():
+    """ablmc_accumulate_levels (one device batch, one synchronisation; what
+    the MLMC driver's allocation rounds use) == one accumulate_samples per
+    level, bit for bit, incl. a multi-super-block level and a no-op."""
+    pr = ablmc.Problem.make(ablmc.ModelParams(), Ig.baoab, ablmc.QoISpec(), 0.5, 0.1, 1.0, 1, 3)
+    reqs = [(0, 0, 70000), (3, 11, 5 * capi.ABLMC_SUPERBLOCK // 2), (1, 5, 0), (6, 0, 4097)]
+    seq, bat = [], []
+    for level, first, count in reqs:
+        a = ablmc.LevelStats().init(level, pr.h_level(level), 1)
+        a.sum_y[0], a.n = 1.25, 7  # add-merge into existing sums
+        ablmc.accumulate_samples(a, first, count, pr, level)
+        seq.append(a)
+        b = ablmc.LevelStats().init(level, pr.h_level(level), 1)
+        b.sum_y[0], b.n = 1.25, 7
+        bat.append(b)
+    ablmc.accumulate_levels([(b, f, c, l) for b, (l, f, c) in zip(bat, reqs)], pr)
+    for a, b in zip(seq, bat):
+        assert (a.sum_y.tolist(), a.sum_y2.tolist(), a.n, a.failed, a.cost_steps) == (
+            b.sum_y.tolist(), b.sum_y2.tolist(), b.n, b.failed, b.cost_steps)
