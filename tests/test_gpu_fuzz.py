@@ -1,0 +1,77 @@
+"""Randomised parity sweep: seeded random problems (model parameters incl.
+non-power-of-two H and extreme u*, release states, horizons, M0, levels,
+coupling signs, integrators, profiles, uniform and adaptive grids), device
+pairs vs the oracle on the device's elementary functions
+(orc_set_device_math): bit-identical states, parities, reflection counts and
+failure flags for every sample.  Exercises the fast path, its exact fallback
+(misses from non-tame parameters, u0 = 0, multiple reflections) and the
+adaptive schedule on inputs no hand-written case covers."""
+import numpy as np
+import pytest
+
+import oracle_lib as O
+from paper_1612_07717_b200 import ablmc
+
+pytestmark = pytest.mark.gpu
+Ig = ablmc.Integrator
+
+
+def random_problem(rng):
+    H = float(rng.choice([1.0, 1.0, 2.0, 3.0, 0.75]))
+    mp = ablmc.ModelParams(kappa_sigma=float(rng.uniform(0.8, 2.0)),
+                           kappa_tau=float(rng.uniform(0.3, 0.9)),
+                           u_star=float(rng.choice([0.1, 0.2, 0.5, 1.0])), H=H,
+                           eps_reg=float(rng.choice([0.005, 0.01, 0.05])) * H,
+                           x_ref=H, noise_scale=float(rng.choice([1.0, 1.0, 0.5, 0.0])))
+    ig = Ig(int(rng.integers(0, 3)))
+    adaptive = bool(rng.random() < 0.3) and ig != Ig.baoab or bool(rng.random() < 0.1)
+    prof = ablmc.Profile.reference
+    kw = {}
+    if not adaptive and rng.random() < 0.25:
+        prof = ablmc.Profile(int(rng.integers(1, 3)))
+        kw = dict(const_sigma_u=1.3, const_tau=float(rng.choice([0.1, 0.5])), sigma_floor=1e-3,
+                  tau_min=1e-3, tau_max=1.0)
+    x0 = float(rng.uniform(0.0, 1.0)) * H
+    u0 = float(rng.choice([0.0, 0.1, -0.3, float(rng.normal(0, 0.5))]))
+    T = float(rng.choice([0.5, 1.0, 2.0]))
+    m0 = int(rng.choice([1, 4, 8, 40]))
+    if ig == Ig.se:
+        m0 = max(m0, 64)  # keep SE mostly below its stability limit
+    level = int(rng.integers(1, 4))
+    opt = ablmc.SampleOptions(signs_on=bool(rng.random() < 0.85), adaptive=adaptive,
+                              x_adapt=float(rng.uniform(0.02, 0.4)) * H)
+    pr = ablmc.Problem.make(mp, ig, ablmc.QoISpec(), x0, u0, T, m0, int(rng.integers(0, 2**40)),
+                            opt, profile=prof, **kw)
+    return pr, level
+
+
+@pytest.mark.parametrize("trial", range(120))
+def test_random_problems_bit_exact_given_device_math(trial):
+    rng = np.random.default_rng(1000 + trial)
+    pr, level = random_problem(rng)
+    c = pr._c
+    n = 48
+    first = int(rng.integers(0, 2**32))
+    got = ablmc.simulate_pairs(pr, level, first, n)
+    M = c.m0 << level
+    O.orc().orc_set_device_math(1)
+    O.orc().orc_set_profile(c.profile, c.const_sigma_u, c.const_tau, c.sigma_floor, c.tau_min,
+                            c.tau_max)
+    try:
+        for i in range(n):
+            if c.adaptive:
+                rc, f, cc, _ = O.orc_pair_adaptive(c.integrator, c.params, c.x0, c.u0, c.T,
+                                                   c.T / M, c.x_adapt, c.seed, level, first + i,
+                                                   c.signs_on)
+            else:
+                rc, f, cc = O.orc_pair(c.integrator, c.params, c.x0, c.u0, c.T, M, c.seed, level,
+                                       first + i, signs_on=c.signs_on)
+            g = got[i]
+            assert (rc == 0) == bool(g["fok"]), (trial, i)
+            if rc == 0:
+                assert ([g["fx"], g["fu"], g["fpar"], g["fn"], g["cx"], g["cu"], g["cpar"],
+                         g["cn"]] == [f.x, f.u, f.parity, f.n_refl, cc.x, cc.u, cc.parity,
+                                      cc.n_refl]), (trial, i)
+    finally:
+        O.orc().orc_set_device_math(0)
+        O.orc().orc_set_profile(0, 0, 0, 0, 0, 0)
