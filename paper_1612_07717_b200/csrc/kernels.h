@@ -61,6 +61,15 @@ struct KernelArgs {
   long long* ad_steps;      // steps taken, -1 = failed sample
   unsigned long long* ad_ctrl;
   long long* ad_redo;       // samples whose fast path missed (recomputed exactly)
+  // single-pass merge inside the sampler launch: tile -> 4096-sample block ->
+  // super-block partials (merge_tail), arrival counters zero between launches
+  double* blk_sums;
+  long long* blk_cnt;
+  double* sb_sums;
+  long long* sb_cnt;
+  unsigned* arr_blk;
+  unsigned* arr_sb;
+  int64_t sb_out;           // super-block row of this launch's first super-block
 };
 
 struct StateOut {
@@ -79,11 +88,8 @@ cudaError_t launch_adaptive_level(const KernelArgs& a, int ig, bool coupled, dou
                                   long long* tile_cnt, cudaStream_t st);
 cudaError_t launch_adaptive_states(const KernelArgs& a, int ig, bool coupled, StateOut* out,
                                    cudaStream_t st);
-cudaError_t launch_binned(const KernelArgs& a, bool coupled, double* tile_sums, cudaStream_t st);
-cudaError_t launch_merge_tiles(int64_t n_tiles, int dim, const double* ts, const long long* tc,
-                               double* bs, long long* bc, cudaStream_t st);
-cudaError_t launch_merge_blocks(int64_t n_blk, int dim, const double* bs, const long long* bc,
-                                double* ss, long long* sc, int64_t sb_base, cudaStream_t st);
+cudaError_t launch_binned(const KernelArgs& a, bool coupled, double* tile_sums,
+                          const long long* tile_cnt, cudaStream_t st);
 cudaError_t launch_merge_super(int64_t n_sb, int dim, const double* ss, const long long* sc,
                                double* rs, long long* rc, cudaStream_t st);
 cudaError_t launch_normals(uint32_t k0, uint32_t k1, uint64_t idx, uint64_t kstart, int64_t n,

@@ -230,6 +230,64 @@ __device__ __forceinline__ void tile_reduce(bool active, bool good, double y, lo
   }
 }
 
+// Single-pass merge, run by every CTA after its tile partial is written:
+// the last CTA of a 4096-sample block (arrival counter) sums the block's
+// tile partials in tile order, and the last block of a super-block sums the
+// block partials in block order -- the same fixed sequential orders as a
+// separate tile->block->super-block reduction, without two extra launches.
+// Counters reset themselves for the next launch.
+__device__ __forceinline__ void merge_tail(const KernelArgs& a, const double* tile_sums,
+                                           const long long* tile_cnt, int dim2) {
+  __shared__ int s_last;
+  __threadfence();  // this CTA's tile partial, visible device-wide
+  __syncthreads();
+  const int64_t n_tiles = (a.n + kTile - 1) / kTile;
+  const int64_t blk = blockIdx.x / ABLMC_TILES_PER_BLOCK;
+  const int64_t t0 = blk * ABLMC_TILES_PER_BLOCK;
+  const int64_t t1 = min(t0 + int64_t(ABLMC_TILES_PER_BLOCK), n_tiles);
+  if (threadIdx.x == 0) s_last = atomicAdd(a.arr_blk + blk, 1u) == unsigned(t1 - t0 - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int c = threadIdx.x; c < dim2 + kCnt; c += blockDim.x) {
+    if (c < dim2) {
+      double v = 0.0;
+      for (int64_t t = t0; t < t1; ++t) v = add(v, __ldcg(tile_sums + t * dim2 + c));
+      a.blk_sums[blk * dim2 + c] = v;
+    } else {
+      long long v = 0;
+      for (int64_t t = t0; t < t1; ++t) v += __ldcg(tile_cnt + kCnt * t + (c - dim2));
+      a.blk_cnt[kCnt * blk + (c - dim2)] = v;
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  const int64_t n_blk = (n_tiles + ABLMC_TILES_PER_BLOCK - 1) / ABLMC_TILES_PER_BLOCK;
+  const int64_t sb = blk / ABLMC_BLOCKS_PER_SUPER;
+  const int64_t b0 = sb * ABLMC_BLOCKS_PER_SUPER;
+  const int64_t b1 = min(b0 + int64_t(ABLMC_BLOCKS_PER_SUPER), n_blk);
+  if (threadIdx.x == 0) {
+    a.arr_blk[blk] = 0u;
+    s_last = atomicAdd(a.arr_sb + sb, 1u) == unsigned(b1 - b0 - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int64_t so = a.sb_out + sb;
+  for (int c = threadIdx.x; c < dim2 + kCnt; c += blockDim.x) {
+    if (c < dim2) {
+      double v = 0.0;
+      for (int64_t b = b0; b < b1; ++b) v = add(v, __ldcg(a.blk_sums + b * dim2 + c));
+      a.sb_sums[so * dim2 + c] = v;
+    } else {
+      long long v = 0;
+      for (int64_t b = b0; b < b1; ++b) v += __ldcg(a.blk_cnt + kCnt * b + (c - dim2));
+      a.sb_cnt[kCnt * so + (c - dim2)] = v;
+    }
+  }
+  if (threadIdx.x == 0) a.arr_sb[sb] = 0u;
+}
+
 // QoI value of one successful sample (qoi.hpp:171-188; the difference for a
 // coupled pair, coupling.hpp:262-268).
 template <bool COUPLED>
