@@ -453,6 +453,18 @@ int64_t ref_result_json(const ablmc_run_config* c, const ablmc_run_result* r, in
   return emit(to_json(rec).dump(2) + "\n", buf, cap);
 }
 
+// output_record_from_json (output.hpp:125-159) then to_json again: the
+// reference's own read-back of a result.json; -1 on a reader exception.
+int64_t ref_result_json_roundtrip(const char* text, char* buf, int64_t cap) {
+  try {
+    const OutputRecord rec = output_record_from_json(nlohmann::ordered_json::parse(text));
+    return emit(to_json(rec).dump(2) + "\n", buf, cap);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 int64_t ref_variance_decay_csv(const ablmc_decay_row* rows, int n, char* buf, int64_t cap) {
   std::vector<DecayRow> v;
   for (int i = 0; i < n; ++i)

@@ -621,6 +621,28 @@ def result_json(cfg: RunConfig, r: RunResult) -> str:
     return _text(lib().ablmc_result_json, _P(cc), _P(r.c), len(r.estimate))
 
 
+def read_result_json(text: str) -> tuple:
+    """output_record_from_json (output.hpp:47-81,125-159): (RunConfig, RunResult)
+    from result.json text -- reload the per-level sums to resume a run."""
+    d = C.c_int64()
+    raw = text.encode()
+    rc = lib().ablmc_read_result_json(raw, None, None, C.byref(d), None, 0)
+    if rc != 0:
+        msg = lib().ablmc_read_result_json_error().decode()
+        raise RuntimeError(msg) if rc == capi.ABLMC_ERR_RUNTIME else ValueError(msg)
+    r, keep = _new_result(int(d.value))
+    k = capi.RunConfigC()
+    buf = C.create_string_buffer(4096)
+    _check(lib().ablmc_read_result_json(raw, _P(k), _P(r), C.byref(d), buf, 4096))
+    m = k.model
+    cfg = RunConfig(ModelParams(m.kappa_sigma, m.kappa_tau, m.u_star, m.H, m.eps_reg, m.x_ref,
+                                m.noise_scale), Method(k.method), Integrator(k.integrator),
+                    QoIKind(k.qoi_kind), k.qoi_a, k.qoi_b, k.qoi_r, k.qoi_delta, k.qoi_bins, k.T,
+                    k.m0, k.eps, k.fixed_n, k.seed, k.x0, k.u0, bool(k.adaptive), k.x_adapt,
+                    bool(k.coupling_signs), k.workers, bool(k.timings), buf.value.decode())
+    return cfg, _result(r, keep)
+
+
 def write_result_json(cfg: RunConfig, r: RunResult, directory) -> str:
     from pathlib import Path
     d = Path(directory)

@@ -173,6 +173,9 @@ SIGNATURES = {
     "ablmc_run_config_defaults": (None, [P(RunConfigC)]),
     "ablmc_result_json": (C.c_int64, [P(RunConfigC), P(RunResultC), C.c_int64, C.c_char_p,
                                       C.c_int64]),
+    "ablmc_read_result_json": (C.c_int, [C.c_char_p, P(RunConfigC), P(RunResultC), P(C.c_int64),
+                                         C.c_char_p, C.c_int64]),
+    "ablmc_read_result_json_error": (C.c_char_p, []),
     "ablmc_variance_decay_csv": (C.c_int64, [P(DecayRowC), C.c_int, C.c_char_p, C.c_int64]),
     "ablmc_cost_sweep_csv": (C.c_int64, [P(CostRowC), C.c_int, C.c_int, C.c_char_p, C.c_int64]),
     "ablmc_pdf_csv": (C.c_int64, [P(C.c_double), C.c_int, P(C.c_double), P(C.c_double),

@@ -2,8 +2,10 @@
 // schema v1 and the CSV tables, byte-identical to the reference's
 // output.hpp:17-225 (same key order and types through nlohmann::ordered_json,
 // dump(2) + "\n"; CSV floats "%.17g").  Host-only C++.
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
@@ -98,6 +100,25 @@ json record_json(const ablmc_run_config& c, const ablmc_run_result& r, int64_t d
   return j;
 }
 
+int method_from(const std::string& v) {  // estimators.hpp:165-172
+  if (v == "stmc") return 0;
+  if (v == "mlmc") return 1;
+  throw std::invalid_argument("unknown method '" + v + "'");
+}
+int integrator_from(const std::string& v) {  // integrators.hpp:14-21
+  if (v == "se") return ABLMC_SE;
+  if (v == "gl") return ABLMC_GL;
+  if (v == "baoab") return ABLMC_BAOAB;
+  throw std::invalid_argument("unknown integrator '" + v + "'");
+}
+int qoi_from(const std::string& v) {  // qoi.hpp:96-104
+  for (int k = ABLMC_QOI_MEAN_POSITION; k <= ABLMC_QOI_BINNED_FIELD; ++k)
+    if (v == qoi_name(k)) return k;
+  throw std::invalid_argument("unknown qoi kind '" + v + "'");
+}
+
+thread_local std::string g_read_error;
+
 std::string fmt(double v) {  // output.hpp:169-173
   char b[40];
   std::snprintf(b, sizeof b, "%.17g", v);
@@ -150,6 +171,115 @@ int64_t ablmc_result_json(const ablmc_run_config* c, const ablmc_run_result* r, 
     return -1;
   }
 }
+
+// output.hpp:47-81 (config_from_json) + 125-159 (output_record_from_json)
+int ablmc_read_result_json(const char* text, ablmc_run_config* cfg, ablmc_run_result* out,
+                           int64_t* dim, char* output_dir, int64_t cap) {
+  if (!text) return ABLMC_ERR_INVALID_ARGUMENT;
+  try {
+    const json j = json::parse(text);
+    const int schema = j.at("schema_version");
+    if (schema != 1)
+      throw std::runtime_error("result file has schema version " + std::to_string(schema) +
+                               ", this reader expects 1");
+    const auto& res = j.at("result");
+    const auto est = res.at("estimate").get<std::vector<double>>();
+    const int64_t d = int64_t(est.size());
+    if (dim) *dim = d;
+    const auto& jc = j.at("config");
+    const std::string dir = jc.at("output").at("dir").get<std::string>();
+    ablmc_run_config local;
+    if (!cfg) cfg = &local;  // parsed (and so validated) either way
+    {
+      ablmc_run_config_defaults(cfg);
+      const auto& m = jc.at("model");
+      cfg->model = {m.at("kappa_sigma"), m.at("kappa_tau"), m.at("u_star"), m.at("h"),
+                    m.at("eps_reg"),     m.at("x_ref"),     m.at("noise_scale")};
+      const auto& r = jc.at("run");
+      cfg->method = method_from(r.at("method").get<std::string>());
+      cfg->integrator = integrator_from(r.at("integrator").get<std::string>());
+      cfg->T = r.at("t");
+      cfg->m0 = r.at("m0");
+      cfg->eps = r.at("eps");
+      cfg->fixed_n = r.at("n_samples");
+      cfg->seed = r.at("seed");
+      cfg->x0 = r.at("x0");
+      cfg->u0 = r.at("u0");
+      cfg->adaptive = r.at("adaptive").get<bool>() ? 1 : 0;
+      cfg->x_adapt = r.at("x_adapt");
+      cfg->coupling_signs = r.at("coupling_signs").get<bool>() ? 1 : 0;
+      cfg->workers = r.at("workers");
+      cfg->timings = r.at("timings").get<bool>() ? 1 : 0;
+      const auto& q = jc.at("qoi");
+      cfg->qoi_kind = qoi_from(q.at("kind").get<std::string>());
+      cfg->qoi_a = q.at("a");
+      cfg->qoi_b = q.at("b");
+      cfg->qoi_r = q.at("r");
+      cfg->qoi_delta = q.at("delta");
+      cfg->qoi_bins = q.at("bins");
+      cfg->output_dir = output_dir;
+    }
+    if (output_dir && cap > 0) emit(dir, output_dir, cap);
+    ablmc_run_result local_out;
+    if (!out) {
+      std::memset(&local_out, 0, sizeof local_out);
+      out = &local_out;  // parsed (and so validated) either way
+    }
+    {
+      const auto err = res.at("stat_error").get<std::vector<double>>();
+      out->estimate = d > 0 ? est[0] : 0.0;
+      out->stat_error = err.empty() ? 0.0 : err[0];
+      if (out->est_vec) std::copy(est.begin(), est.end(), out->est_vec);
+      if (out->err_vec) std::copy(err.begin(), err.end(), out->err_vec);
+      out->bias_estimate = res.at("bias_estimate");
+      out->alpha = res.at("alpha");
+      out->c1 = res.at("c1");
+      out->levels_used = res.at("levels_used");
+      out->total_cost_steps = res.at("total_cost_steps");
+      out->pilot_cost_steps = res.at("pilot_cost_steps");
+      out->failed_samples = res.at("failed_samples");
+      out->warnings_mask = 0;
+      out->n_warnings = 0;
+      for (const auto& w : res.at("warnings")) {
+        const std::string ws = w.get<std::string>();
+        if (ws.rfind("Var[Y_1] >= Var[Y_0]/2", 0) == 0) out->warnings_mask |= 1;
+        else if (ws.rfind("sample allocation did not converge", 0) == 0) out->warnings_mask |= 2;
+        else throw std::invalid_argument("unknown warning '" + ws + "'");
+        ++out->n_warnings;
+      }
+      const auto& levels = res.at("levels");
+      if (levels.size() > size_t(ABLMC_MAX_LEVELS))
+        throw std::invalid_argument("more levels than ABLMC_MAX_LEVELS");
+      out->n_levels = int(levels.size());
+      int l = 0;
+      for (const auto& lv : levels) {
+        out->level_h[l] = lv.at("h");
+        out->level_n[l] = lv.at("n");
+        out->level_failed[l] = lv.at("failed");
+        out->level_cost[l] = lv.at("cost_steps");
+        const auto sy = lv.at("sum_y").get<std::vector<double>>();
+        const auto sy2 = lv.at("sum_y2").get<std::vector<double>>();
+        if (int64_t(sy.size()) != d || int64_t(sy2.size()) != d)
+          throw std::invalid_argument("level sums do not match the estimate's dimension");
+        out->level_sum_y[l] = sy[0];
+        out->level_sum_y2[l] = sy2[0];
+        if (out->level_sum_y_vec) std::copy(sy.begin(), sy.end(), out->level_sum_y_vec + l * d);
+        if (out->level_sum_y2_vec) std::copy(sy2.begin(), sy2.end(), out->level_sum_y2_vec + l * d);
+        ++l;
+      }
+      out->wall_seconds = j.at("timings").at("wall_seconds");
+    }
+    return 0;
+  } catch (const std::runtime_error& e) {
+    g_read_error = e.what();
+    return ABLMC_ERR_RUNTIME;
+  } catch (const std::exception& e) {
+    g_read_error = e.what();
+    return ABLMC_ERR_INVALID_ARGUMENT;
+  }
+}
+
+const char* ablmc_read_result_json_error(void) { return g_read_error.c_str(); }
 
 int64_t ablmc_variance_decay_csv(const ablmc_decay_row* rows, int n, char* buf, int64_t cap) {
   std::string s = "level,h,var_Y,mean_Y,n_samples,cost_steps\n";  // output.hpp:184-191

@@ -99,3 +99,40 @@ def test_csv_writers_byte_identical():
     e = (C.c_double * 65)(*edges)
     assert ablmc.pdf_csv(edges, conc, se) == ref_text(R.ref_pdf_csv, e, 65, (C.c_double * 64)(*conc),
                                                       (C.c_double * 64)(*se))
+
+
+@pytest.mark.parametrize("case", range(8))
+def test_result_json_read_back(case):
+    """output_record_from_json (output.hpp:47-81,125-159): the product reads a
+    result.json back to the same record (re-emitted text byte-identical), and
+    the reference's own reader agrees byte for byte (the resume path: per-level
+    sums reloaded, sampling continues at index n + failed)."""
+    rng = np.random.default_rng(100 + case)
+    dim = [1, 1, 20, 64, 1, 3, 1, 8][case]
+    cfg = ablmc.RunConfig(method=ablmc.Method(case % 2), integrator=ablmc.Integrator(case % 3),
+                          qoi_kind=ablmc.QoIKind.binned_field if dim > 1 else ablmc.QoIKind.smoothed_indicator,
+                          qoi_bins=max(dim, 20), eps=TRICKY[case + 2], seed=2**64 - 1 - case,
+                          m0=40 << case, fixed_n=case * 1000, timings=bool(case % 3),
+                          adaptive=case == 5, coupling_signs=case != 4, workers=case + 1,
+                          output_dir=f"out/{case}", x0=0.05 * (case + 1), u0=-0.1 * case)
+    r, keep = synthetic_result(dim, 1 + case % 5, rng, case % 4)
+    cc = cfg.c()
+    text = ablmc._text(ablmc.lib().ablmc_result_json, C.byref(cc), C.byref(r), dim)
+    cfg2, res2 = ablmc.read_result_json(text)
+    assert cfg2 == cfg
+    assert len(res2.estimate) == dim and len(res2.level_stats) == 1 + case % 5
+    assert ablmc.result_json(cfg2, res2) == text
+    if R is not None:
+        assert ref_text(R.ref_result_json_roundtrip, text.encode()) == text
+
+
+def test_result_json_reader_errors():
+    cfg = ablmc.RunConfig()
+    r, keep = synthetic_result(1, 2, np.random.default_rng(0), 0)
+    text = ablmc._text(ablmc.lib().ablmc_result_json, C.byref(cfg.c()), C.byref(r), 1)
+    with pytest.raises(RuntimeError, match="schema version 2"):
+        ablmc.read_result_json(text.replace('"schema_version": 1', '"schema_version": 2'))
+    with pytest.raises(ValueError):
+        ablmc.read_result_json(text.replace('"gl"', '"rk4"'))
+    with pytest.raises(ValueError):
+        ablmc.read_result_json("{not json")
