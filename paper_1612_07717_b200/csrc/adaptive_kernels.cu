@@ -178,7 +178,7 @@ __device__ __forceinline__ void leg_push(ALeg& L, PendLocal& P, double xi_s, dou
 // the pending increment of a GL/BAOAB leg about to step (register version)
 template <int IG>
 __device__ __forceinline__ void leg_settle(ALeg& L, const PendLocal& P) {
-  if (IG != kSE && L.np <= kPendLocal)
+  if (IG != kSE && L.np >= 3 && L.np <= kPendLocal)  // <= 2: Horner == backward sum
     L.acc = backward_sum(L.np, [&](int r) { return P.t[r]; }, [&](int r) { return P.e[r]; });
 }
 
@@ -450,7 +450,8 @@ __device__ __forceinline__ bool pair_event(PairSM& S, LegStore& st, PendSpill& s
   }
   const int leg = take_fine ? 0 : 1;
   ALeg W = leg_load(st, leg, take_fine ? S.f : S.c);
-  if (IG != kSE && W.np <= kPendLocal) {
+  // (<= 2 pending terms: the Horner form already equals the backward sum)
+  if (IG != kSE && W.np >= 3 && W.np <= kPendLocal) {
     const int i = threadIdx.x;
     W.acc = backward_sum(
         W.np, [&](int r) { return r < kPend ? st.pt[r][leg][i] : sp.t[leg][r - kPend]; },
