@@ -59,7 +59,7 @@ double orc_bits_to_unit(uint32_t hi, uint32_t lo) {
 
 /* ---------------------------------------------------- device-math mode
  * NOT the reference: a restatement of this project's device elementary
- * functions (paper_1612_07717_b200/csrc/ablmc_device.cuh log_unit,
+ * functions (paper_1612_07717_b200/csrc/ablmc_device.cuh log_unit_tab,
  * sincos_2pi, expm1_exp_core and the expm1(2x) = em1 (em1 + 2) identity),
  * with the same explicit FMAs, so tests can drive the oracle with the
  * device's exact log/sin/cos/exp/expm1 and require bit-identical paths for
@@ -71,10 +71,6 @@ static uint64_t dbits(double v) { uint64_t b; memcpy(&b, &v, 8); return b; }
 static double bitsd(uint64_t b) { double v; memcpy(&v, &b, 8); return v; }
 static int lo_int(double v) { return (int)(int32_t)(uint32_t)dbits(v); }
 
-static const double kLg[7] = {6.666666666666735130e-01, 3.999999999940941908e-01,
-                              2.857142874366239149e-01, 2.222219843214978396e-01,
-                              1.818357216161805012e-01, 1.531383769920937332e-01,
-                              1.479819860511658591e-01};
 static const double kS[6] = {-1.66666666666666324348e-01, 8.33333333332248946124e-03,
                              -1.98412698298579493134e-04, 2.75573137070700676789e-06,
                              -2.50507602534068634195e-08, 1.58969099521155010221e-10};
@@ -90,25 +86,47 @@ static const double kEP[12] = {1.0 / 2, 1.0 / 6, 1.0 / 24, 1.0 / 120, 1.0 / 720,
 static const double kER[4] = {1.44269504088896338700e+00, 6.93147180369123816490e-01,
                               1.90821492927058770002e-10, 6755399441055744.0};
 
+/* device log_unit_tab: Tang's table method (see ablmc_device.cuh), the same
+ * table built by the same code as the library's upload_log_table */
+static double dm_invc[256], dm_thi[256], dm_tlo[256];
+static int dm_tab_built = 0;
+static void dm_build_log_table(void) {
+  for (int j = 0; j < 256; ++j) {
+    const int e = j >> 7, b = j & 0x7f;
+    const double lo = (e ? 1.0 : 0.5) * (1.0 + b / 128.0);
+    const double hi = (e ? 1.0 : 0.5) * (1.0 + (b + 1) / 128.0);
+    double c = 0.5 * (lo + hi);
+    if (lo == 1.0 || hi == 1.0) c = 1.0;
+    const double invc = (c == 1.0) ? 1.0 : 1.0 / c;
+    const long double L = -logl((long double)invc);
+    const double th = (double)L;
+    dm_invc[j] = invc;
+    dm_thi[j] = th;
+    dm_tlo[j] = (double)(L - (long double)th);
+  }
+  dm_tab_built = 1;
+}
+static const double kQ[7] = {-1.0 / 2, 1.0 / 3, -1.0 / 4, 1.0 / 5, -1.0 / 6, 1.0 / 7, -1.0 / 8};
+
 static double dm_log_unit(double u) {
+  if (!dm_tab_built) dm_build_log_table();
   const uint64_t b = dbits(u);
   int32_t hx = (int32_t)(b >> 32);
   int k = (hx >> 20) - 1023;
   hx &= 0x000fffff;
   const int i = (hx + 0x95f64) & 0x100000;
-  const double mnt = bitsd(((uint64_t)(uint32_t)(hx | (i ^ 0x3ff00000)) << 32) | (uint32_t)b);
+  const int32_t mhi = hx | (i ^ 0x3ff00000);
+  const double mnt = bitsd(((uint64_t)(uint32_t)mhi << 32) | (uint32_t)b);
   k += i >> 20;
-  const double f = mnt - 1.0;
-  const double hfsq = (0.5 * f) * f;
-  const double sq = f / (2.0 + f);
-  const double z = sq * sq;
-  const double w = z * z;
-  const double p1 = fma(w, fma(w, kLg[5], kLg[3]), kLg[1]);
-  const double t2 = z * fma(w, fma(w, fma(w, kLg[6], kLg[4]), kLg[2]), kLg[0]);
-  const double R = fma(w, p1, t2);
+  const int j = ((mhi >> 13) & 0x7f) | ((mhi >> 13) & 0x80);
+  const double r = fma(mnt, dm_invc[j], -1.0);
+  const double r2 = r * r;
+  double q = kQ[6];
+  for (int t = 5; t >= 0; --t) q = fma(q, r, kQ[t]);
   const double dk = (double)k;
-  const double inner = fma(sq, hfsq + R, dk * kBm[1]);
-  return fma(dk, kBm[0], -((hfsq - inner) - f));
+  const double hi = fma(dk, kBm[0], dm_thi[j]);
+  const double lo = fma(dk, kBm[1], dm_tlo[j]);
+  return hi + (r + fma(r2, q, lo));
 }
 
 static void dm_sincos_2pi(double th, double* sn, double* cs) {

@@ -699,6 +699,8 @@ cudaError_t states_p(const KernelArgs& a, bool coupled, StateOut* out, cudaStrea
 
 }  // namespace
 
+cudaError_t upload_log_table_adaptive() { return upload_log_table_here(); }
+
 cudaError_t launch_adaptive_level(const KernelArgs& a, int ig, bool coupled, double* tile_sums,
                                   long long* tile_cnt, cudaStream_t st) {
   switch (ig) {

@@ -92,6 +92,8 @@ cudaError_t launch_binned(const KernelArgs& a, bool coupled, double* tile_sums,
                           const long long* tile_cnt, cudaStream_t st);
 cudaError_t launch_merge_super(int64_t n_sb, int dim, const double* ss, const long long* sc,
                                double* rs, long long* rc, cudaStream_t st);
+cudaError_t upload_log_table();           // Box-Muller log table (ablmc_init), one
+cudaError_t upload_log_table_adaptive();  // per translation unit that draws normals
 cudaError_t launch_normals(uint32_t k0, uint32_t k1, uint64_t idx, uint64_t kstart, int64_t n,
                            double* out, cudaStream_t st);
 // DFMA throughput probe (FP64 lane-ops/s), see ablmc_probe_fp64_rate.
