@@ -558,3 +558,25 @@ def test_accumulate_levels_batch_equals_sequential_calls():
     for a, b in zip(seq, bat):
         assert (a.sum_y.tolist(), a.sum_y2.tolist(), a.n, a.failed, a.cost_steps) == (
             b.sum_y.tolist(), b.sum_y2.tolist(), b.n, b.failed, b.cost_steps)
+
+
+@pytest.mark.parametrize("x0,u0", [(0.5, float("nan")), (0.5, float("inf")), (1.5, 0.1),
+                                   (11.0, 0.0), (0.0, -0.2), (1.0, 0.3)])
+def test_degenerate_release_states_like_the_reference(x0, u0):
+    """Release states the reference does not validate (model.hpp has no check
+    on x0/u0): non-finite velocities fail every sample through reflect's
+    finiteness test (particle.hpp:38-39), a release outside [0, H] is
+    reflected on the first step or, beyond 10 H, fails; releases on the walls
+    are inside.  Device == oracle (counts exact, sums within 1e-11)."""
+    for ig in Ig:
+        pr = ablmc.Problem.make(ablmc.ModelParams(), ig, ablmc.QoISpec(), x0, u0, 1.0, 40, 9)
+        for level in (0, 2):
+            acc = ablmc.LevelStats().init(level, pr.h_level(level), 1)
+            ablmc.accumulate_samples(acc, 0, 3000, pr, level)
+            st = O.Stats(1)
+            assert O.orc().orc_accumulate_samples(C.byref(pr._c), level, 0, 3000,
+                                                  C.byref(st.c)) == 0
+            assert (acc.n, acc.failed, acc.cost_steps) == (st.n, st.failed, st.cost_steps), (
+                ig, level)
+            if st.n:
+                assert close(acc.sum_y, st.sum_y, 1e-11, 1e-13)
