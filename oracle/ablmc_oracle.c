@@ -66,6 +66,9 @@ double orc_bits_to_unit(uint32_t hi, uint32_t lo) {
  * every integrator.  The reference's own math (glibc) stays the default. */
 static __thread int g_devmath = 0;
 void orc_set_device_math(int on) { g_devmath = on; }
+/* diagnostics: the largest pending-sub-interval count of the last adaptive pair */
+static __thread int g_max_pending;
+int orc_last_max_pending(void) { return g_max_pending; }
 
 static uint64_t dbits(double v) { uint64_t b; memcpy(&b, &v, 8); return b; }
 static double bitsd(uint64_t b) { double v; memcpy(&v, &b, 8); return v; }
@@ -530,6 +533,7 @@ int orc_simulate_pair_adaptive(int ig, const ablmc_model_params* p, double x0, d
   f->s = (orc_state){x0, u0, +1, 0};
   f->t = 0.0; f->done = 0; f->steps = 0; f->n = 0;
   *c = *f;
+  g_max_pending = 0;
   leg_schedule(f, h_base, T, x_adapt, p);
   leg_schedule(c, 2.0 * h_base, T, x_adapt, p);
   const int64_t max_iter = 256 * (int64_t)ceil(T / h_base) + 256;
@@ -553,6 +557,8 @@ int orc_simulate_pair_adaptive(int ig, const ablmc_model_params* p, double x0, d
         c->xi[c->n] = xi; c->dt[c->n] = dt; c->lam[c->n] = orc_sde_coeffs(c->s.x, p).lambda;
         c->sg[c->n++] = sf;
       }
+      if (f->n > g_max_pending) g_max_pending = f->n;
+      if (c->n > g_max_pending) g_max_pending = c->n;
     }
     if (!f->done && f->t_next == tau_next) {
       if (leg_take(ig, f, 0, p)) { rc = -1; break; }

@@ -609,9 +609,9 @@ __global__ void __launch_bounds__(kTile) k_adaptive_tiles(const KernelArgs a,
   const bool binned = a.qoi_kind == 3;
   const long long steps = active ? a.ad_steps[j] : 0;
   const bool good = active && steps >= 0;
-  tile_reduce(active, good, (good && !binned) ? a.ad_y[j] : 0.0, steps, binned, tile_sums,
-              tile_cnt);
-  if (!binned) merge_tail(a, tile_sums, tile_cnt, 2);
+  tile_prologue();
+  tile_reduce<false>(a, active, good, (good && !binned) ? a.ad_y[j] : 0.0, steps, binned,
+                     tile_sums, tile_cnt);
 }
 
 template <int IG, int PROF, bool COUPLED>

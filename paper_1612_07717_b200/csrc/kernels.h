@@ -21,6 +21,9 @@ constexpr int kCnt = 3;
 #ifndef ABLMC_MINB_GL
 #define ABLMC_MINB_GL 3
 #endif
+#ifndef ABLMC_MINB_PATH
+#define ABLMC_MINB_PATH 5
+#endif
 #ifndef ABLMC_MINB_BAOAB
 #define ABLMC_MINB_BAOAB 3
 #endif

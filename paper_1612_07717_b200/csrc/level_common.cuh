@@ -172,55 +172,172 @@ __device__ __forceinline__ double g_edge(double x, int e, int k, const double* e
 }
 
 // Resident CTAs per SM requested from ptxas (register budget 65536 / (256 *
-// blocks)); tuned per integrator against spills.
-template <int IG>
+// blocks)); tuned per integrator against spills.  The
+// single-path kernels (level 0, StMC: no coarse leg) fit fewer registers.
+template <int IG, bool COUPLED = true>
 struct MinBlocks {
-  static constexpr int value = IG == kSE ? ABLMC_MINB_SE : (IG == kGL ? ABLMC_MINB_GL : ABLMC_MINB_BAOAB);
+  static constexpr int value =
+      !COUPLED ? ABLMC_MINB_PATH
+               : (IG == kSE ? ABLMC_MINB_SE : (IG == kGL ? ABLMC_MINB_GL : ABLMC_MINB_BAOAB));
 };
+
+// sum_{i < n} p[i * stride] in index order (the fixed merge order), with the
+// loads issued 16 at a time: the merges at the end of a launch are otherwise
+// one dependent L2 round trip per partial (a 2^22-sample super-block has 1024
+// block partials: ~0.1 ms on the kernel's tail).
+__device__ __forceinline__ double ordered_sum(const double* p, int64_t n, int64_t stride) {
+  double v = 0.0;
+  int64_t i = 0;
+  for (; i + 16 <= n; i += 16) {
+    double x[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) x[k] = __ldcg(p + (i + k) * stride);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v = add(v, x[k]);
+  }
+  for (; i < n; ++i) v = add(v, __ldcg(p + i * stride));
+  return v;
+}
+__device__ __forceinline__ long long ordered_sum(const long long* p, int64_t n, int64_t stride) {
+  long long v = 0;
+  int64_t i = 0;
+  for (; i + 16 <= n; i += 16) {
+    long long x[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) x[k] = __ldcg(p + (i + k) * stride);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v += x[k];
+  }
+  for (; i < n; ++i) v += __ldcg(p + i * stride);
+  return v;
+}
+
+// Per-CTA arrival counter of the tile epilogue (one per CTA; tile_prologue
+// zeroes it before any warp can arrive).
+__device__ __forceinline__ unsigned& tile_arrivals() {
+  __shared__ unsigned s_arrive;
+  return s_arrive;
+}
+__device__ __forceinline__ void tile_prologue() {
+  if (threadIdx.x == 0) tile_arrivals() = 0u;
+  __syncthreads();
+}
+
+// Block / super-block merge of the tile partials, run by ONE warp (the last
+// to finish in its CTA) for scalar QoIs (dim2 + kCnt <= 32 values): the last
+// tile of a 4096-sample block (arrival counter) sums the block's tile partials
+// in tile order, the last block of a 2^22-sample super-block sums the block
+// partials in block order -- the fixed sequential orders of merge_tail below.
+__device__ __forceinline__ void merge_tail_warp(const KernelArgs& a, const double* tile_sums,
+                                                const long long* tile_cnt, int dim2) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n_tiles = (a.n + kTile - 1) / kTile;
+  const int64_t blk = blockIdx.x / ABLMC_TILES_PER_BLOCK;
+  const int64_t t0 = blk * ABLMC_TILES_PER_BLOCK;
+  const int64_t t1 = min(t0 + int64_t(ABLMC_TILES_PER_BLOCK), n_tiles);
+  unsigned last = 0;
+  if (lane == 0) {
+    __threadfence();  // lane 0 wrote this tile's partial
+    last = atomicAdd(a.arr_blk + blk, 1u) == unsigned(t1 - t0 - 1);
+  }
+  if (!__shfl_sync(0xffffffffu, last, 0)) return;
+  __threadfence();
+  const int c = lane;
+  if (c < dim2) {
+    a.blk_sums[blk * dim2 + c] = ordered_sum(tile_sums + t0 * dim2 + c, t1 - t0, dim2);
+  } else if (c < dim2 + kCnt) {
+    a.blk_cnt[kCnt * blk + (c - dim2)] = ordered_sum(tile_cnt + kCnt * t0 + (c - dim2), t1 - t0, kCnt);
+  }
+  __threadfence();
+  __syncwarp();
+  const int64_t n_blk = (n_tiles + ABLMC_TILES_PER_BLOCK - 1) / ABLMC_TILES_PER_BLOCK;
+  const int64_t sb = blk / ABLMC_BLOCKS_PER_SUPER;
+  const int64_t b0 = sb * ABLMC_BLOCKS_PER_SUPER;
+  const int64_t b1 = min(b0 + int64_t(ABLMC_BLOCKS_PER_SUPER), n_blk);
+  last = 0;
+  if (lane == 0) {
+    a.arr_blk[blk] = 0u;
+    last = atomicAdd(a.arr_sb + sb, 1u) == unsigned(b1 - b0 - 1);
+  }
+  if (!__shfl_sync(0xffffffffu, last, 0)) return;
+  __threadfence();
+  const int64_t so = a.sb_out + sb;
+  if (c < dim2) {
+    a.sb_sums[so * dim2 + c] = ordered_sum(a.blk_sums + b0 * dim2 + c, b1 - b0, dim2);
+  } else if (c < dim2 + kCnt) {
+    a.sb_cnt[kCnt * so + (c - dim2)] = ordered_sum(a.blk_cnt + kCnt * b0 + (c - dim2), b1 - b0, kCnt);
+  }
+  if (lane == 0) a.arr_sb[sb] = 0u;
+}
 
 // Tile reduction shared by the level kernels: the tile's {sum_y, sum_y2}
 // (fixed warp-shuffle tree, then warps in order) of the successful samples'
 // QoI values y, and counts {n, failed, cost_steps}.  Binned field: sums come
-// from K4, only the counts are reduced here.
-__device__ __forceinline__ void tile_reduce(bool active, bool good, double y, long long steps,
-                                            bool binned, double* __restrict__ tile_sums,
+// from K4, only the counts are reduced here.  No CTA barrier: each warp
+// leaves its partial in shared memory and the LAST warp to arrive (shared
+// arrival counter, zeroed by tile_prologue) sums the warps in order, writes
+// the tile partial and, for scalar QoIs, runs the block/super-block merge;
+// the other warps retire at once (at level 0 the barrier was 27% of the
+// stalls).
+// UNIFORM_STEPS: every successful sample of the tile took `steps` steps (the
+// uniform grids), so the counts are two warp votes; otherwise (adaptive) the
+// step counts are summed by shuffles.  Integer sums: the same values either way.
+template <bool UNIFORM_STEPS>
+__device__ __forceinline__ void tile_reduce(const KernelArgs& a, bool active, bool good, double y,
+                                            long long steps, bool binned,
+                                            double* __restrict__ tile_sums,
                                             long long* __restrict__ tile_cnt) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ double s_red[kWarps][2];
   __shared__ long long s_cnt[kWarps][kCnt];
-  long long cn = good ? 1 : 0, cf = (active && !good) ? 1 : 0, cc = good ? steps : 0;
+  long long cn, cf, cc;
+  if (UNIFORM_STEPS) {
+    cn = __popc(__ballot_sync(0xffffffffu, good));
+    cf = __popc(__ballot_sync(0xffffffffu, active && !good));
+    cc = cn * steps;
+  } else {
+    cn = good ? 1 : 0;
+    cf = (active && !good) ? 1 : 0;
+    cc = good ? steps : 0;
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    cn += __shfl_down_sync(0xffffffffu, cn, off);
-    cf += __shfl_down_sync(0xffffffffu, cf, off);
-    cc += __shfl_down_sync(0xffffffffu, cc, off);
+    for (int off = 16; off > 0; off >>= 1) {
+      cn += __shfl_down_sync(0xffffffffu, cn, off);
+      cf += __shfl_down_sync(0xffffffffu, cf, off);
+      cc += __shfl_down_sync(0xffffffffu, cc, off);
+    }
   }
-  if (lane == 0) {
-    s_cnt[warp][0] = cn;
-    s_cnt[warp][1] = cf;
-    s_cnt[warp][2] = cc;
-  }
+  double sy = 0.0, sy2 = 0.0;
   if (!binned) {
-    double sy = good ? y : 0.0, sy2 = good ? mul(y, y) : 0.0;
+    sy = good ? y : 0.0;
+    sy2 = good ? mul(y, y) : 0.0;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
       sy = add(sy, __shfl_down_sync(0xffffffffu, sy, off));
       sy2 = add(sy2, __shfl_down_sync(0xffffffffu, sy2, off));
     }
-    if (lane == 0) {
-      s_red[warp][0] = sy;
-      s_red[warp][1] = sy2;
-    }
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  unsigned last = 0;
+  if (lane == 0) {
+    s_red[warp][0] = sy;
+    s_red[warp][1] = sy2;
+    s_cnt[warp][0] = cn;
+    s_cnt[warp][1] = cf;
+    s_cnt[warp][2] = cc;
+    __threadfence_block();
+    last = atomicAdd(&tile_arrivals(), 1u) == unsigned(kWarps - 1);
+  }
+  if (!__shfl_sync(0xffffffffu, last, 0)) return;
+  if (lane == 0) {
+    __threadfence_block();
+    const volatile double* vr = &s_red[0][0];
+    const volatile long long* vc = &s_cnt[0][0];
     double ty = 0.0, ty2 = 0.0;
     long long t[kCnt] = {0, 0, 0};
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) {
-      ty = add(ty, s_red[w][0]);
-      ty2 = add(ty2, s_red[w][1]);
-      for (int c = 0; c < kCnt; ++c) t[c] += s_cnt[w][c];
+      ty = add(ty, vr[2 * w]);
+      ty2 = add(ty2, vr[2 * w + 1]);
+      for (int c = 0; c < kCnt; ++c) t[c] += vc[kCnt * w + c];
     }
     if (!binned) {
       tile_sums[2 * blockIdx.x] = ty;  // dim == 1
@@ -228,6 +345,7 @@ __device__ __forceinline__ void tile_reduce(bool active, bool good, double y, lo
     }
     for (int c = 0; c < kCnt; ++c) tile_cnt[kCnt * blockIdx.x + c] = t[c];
   }
+  if (!binned) merge_tail_warp(a, tile_sums, tile_cnt, 2);
 }
 
 // Single-pass merge, run by every CTA after its tile partial is written:
@@ -236,10 +354,13 @@ __device__ __forceinline__ void tile_reduce(bool active, bool good, double y, lo
 // block partials in block order -- the same fixed sequential orders as a
 // separate tile->block->super-block reduction, without two extra launches.
 // Counters reset themselves for the next launch.
+// `writers`: threads [0, writers) wrote this CTA's tile partial; only they
+// need the fence before the arrival atomic (a fence per warp costs ~100s of
+// cycles: at level 0 it was 12% of the kernel's stalls).
 __device__ __forceinline__ void merge_tail(const KernelArgs& a, const double* tile_sums,
-                                           const long long* tile_cnt, int dim2) {
+                                           const long long* tile_cnt, int dim2, int writers = 1) {
   __shared__ int s_last;
-  __threadfence();  // this CTA's tile partial, visible device-wide
+  if (int(threadIdx.x) < writers) __threadfence();  // this CTA's tile partial, visible device-wide
   __syncthreads();
   const int64_t n_tiles = (a.n + kTile - 1) / kTile;
   const int64_t blk = blockIdx.x / ABLMC_TILES_PER_BLOCK;
@@ -250,15 +371,8 @@ __device__ __forceinline__ void merge_tail(const KernelArgs& a, const double* ti
   if (!s_last) return;
   __threadfence();
   for (int c = threadIdx.x; c < dim2 + kCnt; c += blockDim.x) {
-    if (c < dim2) {
-      double v = 0.0;
-      for (int64_t t = t0; t < t1; ++t) v = add(v, __ldcg(tile_sums + t * dim2 + c));
-      a.blk_sums[blk * dim2 + c] = v;
-    } else {
-      long long v = 0;
-      for (int64_t t = t0; t < t1; ++t) v += __ldcg(tile_cnt + kCnt * t + (c - dim2));
-      a.blk_cnt[kCnt * blk + (c - dim2)] = v;
-    }
+    if (c < dim2) a.blk_sums[blk * dim2 + c] = ordered_sum(tile_sums + t0 * dim2 + c, t1 - t0, dim2);
+    else a.blk_cnt[kCnt * blk + (c - dim2)] = ordered_sum(tile_cnt + kCnt * t0 + (c - dim2), t1 - t0, kCnt);
   }
   __threadfence();
   __syncthreads();
@@ -275,15 +389,8 @@ __device__ __forceinline__ void merge_tail(const KernelArgs& a, const double* ti
   __threadfence();
   const int64_t so = a.sb_out + sb;
   for (int c = threadIdx.x; c < dim2 + kCnt; c += blockDim.x) {
-    if (c < dim2) {
-      double v = 0.0;
-      for (int64_t b = b0; b < b1; ++b) v = add(v, __ldcg(a.blk_sums + b * dim2 + c));
-      a.sb_sums[so * dim2 + c] = v;
-    } else {
-      long long v = 0;
-      for (int64_t b = b0; b < b1; ++b) v += __ldcg(a.blk_cnt + kCnt * b + (c - dim2));
-      a.sb_cnt[kCnt * so + (c - dim2)] = v;
-    }
+    if (c < dim2) a.sb_sums[so * dim2 + c] = ordered_sum(a.blk_sums + b0 * dim2 + c, b1 - b0, dim2);
+    else a.sb_cnt[kCnt * so + (c - dim2)] = ordered_sum(a.blk_cnt + kCnt * b0 + (c - dim2), b1 - b0, kCnt);
   }
   if (threadIdx.x == 0) a.arr_sb[sb] = 0u;
 }
@@ -314,8 +421,8 @@ __device__ __forceinline__ void tile_epilogue(const KernelArgs& a, int64_t j, bo
   const bool good = active && o.ok;
   const bool binned = a.qoi_kind == 3;
   if (binned && active) store_pos(a, j, good, o);
-  tile_reduce(active, good, (!binned && good) ? sample_y<COUPLED>(a, o) : 0.0, steps, binned,
-              tile_sums, tile_cnt);
+  tile_reduce<true>(a, active, good, (!binned && good) ? sample_y<COUPLED>(a, o) : 0.0, steps,
+                    binned, tile_sums, tile_cnt);
 }
 
 }  // namespace

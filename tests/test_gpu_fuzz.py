@@ -1,5 +1,6 @@
 """Randomised parity sweep: seeded random problems (model parameters incl.
-non-power-of-two H and extreme u*, release states, horizons, M0, levels,
+non-power-of-two H and extreme u* (1e-12: sigma_U^2 below the fast path's
+2^-59 floor), release states, horizons, M0, levels,
 coupling signs, integrators, profiles, uniform and adaptive grids), device
 pairs vs the oracle on the device's elementary functions
 (orc_set_device_math): bit-identical states, parities, reflection counts and
@@ -14,13 +15,14 @@ from paper_1612_07717_b200 import ablmc
 
 pytestmark = pytest.mark.gpu
 Ig = ablmc.Integrator
+KPEND_LOCAL = 64  # pending sub-intervals a device leg stores (adaptive_kernels.cu kPendLocal)
 
 
 def random_problem(rng):
     H = float(rng.choice([1.0, 1.0, 2.0, 3.0, 0.75]))
     mp = ablmc.ModelParams(kappa_sigma=float(rng.uniform(0.8, 2.0)),
                            kappa_tau=float(rng.uniform(0.3, 0.9)),
-                           u_star=float(rng.choice([0.1, 0.2, 0.5, 1.0])), H=H,
+                           u_star=float(rng.choice([0.1, 0.2, 0.5, 1.0, 1e-12])), H=H,
                            eps_reg=float(rng.choice([0.005, 0.01, 0.05])) * H,
                            x_ref=H, noise_scale=float(rng.choice([1.0, 1.0, 0.5, 0.0])))
     ig = Ig(int(rng.integers(0, 3)))
@@ -68,7 +70,18 @@ def test_random_problems_bit_exact_given_device_math(trial):
                                        first + i, signs_on=c.signs_on)
             g = got[i]
             assert (rc == 0) == bool(g["fok"]), (trial, i)
-            if rc == 0:
+            # GL/BAOAB adaptive legs store up to 64 pending sub-intervals for
+            # the reference's backward sum; beyond that the device uses the
+            # Horner form (adaptive_kernels.cu), equal within rounding: such
+            # samples are held to the north-star 1e-12 instead of bit identity.
+            deep = (c.adaptive and c.integrator != Ig.se
+                    and O.orc().orc_last_max_pending() > KPEND_LOCAL)
+            if rc == 0 and deep:
+                assert [g["fpar"], g["fn"], g["cpar"], g["cn"]] == [
+                    f.parity, f.n_refl, cc.parity, cc.n_refl], (trial, i)
+                for a, b in ((g["fx"], f.x), (g["fu"], f.u), (g["cx"], cc.x), (g["cu"], cc.u)):
+                    assert abs(a - b) <= 1e-12 * max(abs(b), 1e-3), (trial, i, a, b)
+            elif rc == 0:
                 assert ([g["fx"], g["fu"], g["fpar"], g["fn"], g["cx"], g["cu"], g["cpar"],
                          g["cn"]] == [f.x, f.u, f.parity, f.n_refl, cc.x, cc.u, cc.parity,
                                       cc.n_refl]), (trial, i)

@@ -561,7 +561,8 @@ def test_accumulate_levels_batch_equals_sequential_calls():
 
 
 @pytest.mark.parametrize("x0,u0", [(0.5, float("nan")), (0.5, float("inf")), (1.5, 0.1),
-                                   (11.0, 0.0), (0.0, -0.2), (1.0, 0.3)])
+                                   (11.0, 0.0), (0.0, -0.2), (1.0, 0.3), (-0.0, 0.2),
+                                   (-0.0, -0.2), (-1e-300, 0.1)])
 def test_degenerate_release_states_like_the_reference(x0, u0):
     """Release states the reference does not validate (model.hpp has no check
     on x0/u0): non-finite velocities fail every sample through reflect's
