@@ -22,7 +22,10 @@ SOURCES = ["level_kernels.cu", "adaptive_kernels.cu", "binned_kernels.cu", "capi
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = os.environ.get("CXX", "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-I", str(ROOT / "include")]
+# -ffp-contract=off for host code: host_coeffs (capi.cu) must round like the
+# device's IEEE path
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2,-ffp-contract=off", "-I",
+         str(ROOT / "include")]
 # nlohmann/json (header-only, shipped in this image under cudnn_frontend) for
 # byte-identical result.json output (csrc/output.cpp).
 NLOHMANN = Path(os.environ.get(

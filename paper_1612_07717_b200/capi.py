@@ -145,6 +145,7 @@ SIGNATURES = {
     "ablmc_level_kernel_times": (C.c_int, [P(C.c_double), P(C.c_int64)]),
     "ablmc_probe_fp64_rate": (C.c_int, [P(C.c_double)]),
     "ablmc_selftest_fastmath": (C.c_int, [C.c_int64, C.c_uint64, P(C.c_uint64)]),
+    "ablmc_release_coeffs": (C.c_int, [P(ProblemC), P(C.c_double)]),
     "ablmc_pair_states": (C.c_int, [P(ProblemC), C.c_int, C.c_int64, C.c_int64, P(C.c_double),
                                     P(PairStateC)]),
     "ablmc_path_states": (C.c_int, [P(ProblemC), C.c_int64, C.c_uint32, C.c_int64, C.c_int64,

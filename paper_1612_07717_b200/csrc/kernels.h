@@ -32,6 +32,7 @@ constexpr int kCnt = 3;
 struct KernelArgs {
   ablmc_dev::DevModel model;
   double x0, u0;
+  ablmc_dev::Coef c_x0;     // sde_coeffs(x0): every sample's first-step coefficients (host)
   double h, sqrt_h;         // fine step T/M and sqrt(h)
   double h2, sqrt_h2;       // coarse step 2h and sqrt(2h)
   double h_half, h2_half;   // 0.5*h, 0.5*(2h) (BAOAB half steps)

@@ -6,6 +6,8 @@
 
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "ablmc_device.cuh"
 #include "kernels.h"
 
@@ -29,6 +31,12 @@ template <int IG, int PROF, bool COUPLED, bool XI, int FAST>
 __device__ __forceinline__ PathOut run_sample(const KernelArgs& a, uint64_t idx,
                                               const double* __restrict__ xi, bool& bad) {
   const DevModel& m = a.model;
+  // sde_coeffs(x0): every path starts at x0, so the first step's (fine and
+  // coarse) coefficients are launch constants, evaluated once on the host
+  // with the IEEE semantics of this path (capi.cu host_coeffs; the same bits
+  // as coeffs<PROF, FAST>(x0) wherever that raises no miss).
+  Coef cx0 = a.c_x0;
+  cx0.rsu2 = FAST ? recip_fast(cx0.su2) : 0.0;
   PathOut o;
   double u0 = a.u0;
   if (a.random_u0) {
@@ -37,17 +45,18 @@ __device__ __forceinline__ PathOut run_sample(const KernelArgs& a, uint64_t idx,
     double z0, z1;
     normal_pair(uint64_t(a.M) >> 1, idx, a.key, z0, z1);
     const double z = (a.M & 1) ? z1 : z0;
-    u0 = mul(__dsqrt_rn(coeffs<PROF, false>(a.x0, m, bad).su2), z);
+    u0 = mul(__dsqrt_rn(cx0.su2), z);
   }
   o.f = {a.x0, u0, 1, 0};
   o.c = o.f;
   o.ok = true;
   const double h = a.h, sqrt_h = a.sqrt_h;
   if (!COUPLED) {
-    Coef c0;
-    if (IG == kBAOAB) c0 = coeffs<PROF, FAST>(a.x0, m, bad);
+    Coef c0 = cx0;  // BAOAB: sde_coeffs at the current x
     double z0 = 0.0, z1 = 0.0;
-    for (int64_t k = 0; k < a.M; ++k) {
+    // one step; FIRST: at x0 (coefficients cx0)
+    auto step = [&](auto first, int64_t k) -> bool {
+      constexpr bool FIRST = decltype(first)::value;
       double xi_k;
       if (XI) {
         xi_k = xi[k];
@@ -55,33 +64,37 @@ __device__ __forceinline__ PathOut run_sample(const KernelArgs& a, uint64_t idx,
         if ((k & 1) == 0) normal_pair(uint64_t(k) >> 1, idx, a.key, z0, z1);
         xi_k = (k & 1) ? z1 : z0;
       }
-      bool ok;
       if (IG == kSE) {
-        ok = se_step<PROF, FAST>(o.f, h, sqrt_h, xi_k, m, bad);
+        return FIRST ? se_update<FAST>(o.f, cx0, h, sqrt_h, xi_k, m, bad)
+                     : se_step<PROF, FAST>(o.f, h, sqrt_h, xi_k, m, bad);
       } else if (IG == kGL) {
         double e;
-        ok = gl_step<PROF, FAST>(o.f, h, xi_k, m, e, bad);
+        if (FIRST) {
+          double sd;
+          ou_terms<FAST>(cx0.lam, h, e, sd, bad);
+          return gl_update<FAST>(o.f, cx0, h, xi_k, e, sd, m, bad);
+        }
+        return gl_step<PROF, FAST>(o.f, h, xi_k, m, e, bad);
       } else {
         int pm;
-        ok = baoab_step<PROF, FAST>(o.f, c0, h, a.h_half, xi_k, false, pm, m, bad);
+        return baoab_step<PROF, FAST>(o.f, c0, h, a.h_half, xi_k, false, pm, m, bad);
       }
-      if (!ok) o.ok = false;
-      if (!ok || (FAST && bad)) break;
-    }
+    };
+    if (a.M <= 0) return o;
+    bool ok = step(std::true_type{}, 0);  // step 0 peeled (BAOAB: no difference)
+    for (int64_t k = 1; ok && !(FAST && bad) && k < a.M; ++k) ok = step(std::false_type{}, k);
+    o.ok = ok;
     return o;
   }
   const double h2 = a.h2, sqrt_h2 = a.sqrt_h2;
   const bool signs = a.signs_on;
-  Coef cf, cc;  // BAOAB: cached sde_coeffs at the current fine / coarse x
-  if (IG == kBAOAB) {
-    cf = coeffs<PROF, FAST>(a.x0, m, bad);
-    cc = cf;
-  }
-  const int64_t windows = a.M >> 1;
+  Coef cf = cx0, cc = cx0;  // BAOAB: cached sde_coeffs at the current fine / coarse x
   // (Generating the normals one window ahead was measured 12% slower: the
   // scheduler already overlaps Box-Muller with the window's steps, and the
   // extra live registers cost occupancy.)
-  for (int64_t n = 0; n < windows; ++n) {
+  // one window (2 fine steps, 1 coarse step); FIRST: window 0, both legs at x0
+  auto window = [&](auto first, int64_t n) -> bool {
+    constexpr bool FIRST = decltype(first)::value;
     double xi0, xi1;
     if (XI) {
       xi0 = xi[2 * n];
@@ -93,9 +106,10 @@ __device__ __forceinline__ PathOut run_sample(const KernelArgs& a, uint64_t idx,
     if (IG == kSE) {
       // the coarse coefficients do not depend on the fine steps: issued first
       // so the scheduler can interleave the two chains
-      const Coef ccw = coeffs<PROF, FAST>(o.c.x, m, bad);
+      const Coef ccw = FIRST ? cx0 : coeffs<PROF, FAST>(o.c.x, m, bad);
       const int p0 = o.f.par;
-      ok = se_step<PROF, FAST>(o.f, h, sqrt_h, xi0, m, bad);
+      ok = FIRST ? se_update<FAST>(o.f, cx0, h, sqrt_h, xi0, m, bad)
+                 : se_step<PROF, FAST>(o.f, h, sqrt_h, xi0, m, bad);
       const int p1 = o.f.par;
       ok = ok && se_step<PROF, FAST>(o.f, h, sqrt_h, xi1, m, bad);
       const int s0 = signs ? p0 : 1, s1 = signs ? p1 : 1, sc = signs ? o.c.par : 1;
@@ -104,12 +118,24 @@ __device__ __forceinline__ PathOut run_sample(const KernelArgs& a, uint64_t idx,
     } else if (IG == kGL) {
       const int p0 = o.f.par;
       double e0, e1, ec;
-      ok = gl_step<PROF, FAST>(o.f, h, xi0, m, e0, bad);  // e0 = exp(-lam(x_f at window start) h)
+      if (FIRST) {
+        double sd;
+        ou_terms<FAST>(cx0.lam, h, e0, sd, bad);
+        ok = gl_update<FAST>(o.f, cx0, h, xi0, e0, sd, m, bad);
+      } else {
+        ok = gl_step<PROF, FAST>(o.f, h, xi0, m, e0, bad);  // e0 = exp(-lam(x_f at window start) h)
+      }
       const int p1 = o.f.par;
       ok = ok && gl_step<PROF, FAST>(o.f, h, xi1, m, e1, bad);
       const int s0 = signs ? p0 : 1, s1 = signs ? p1 : 1, sc = signs ? o.c.par : 1;
-      ok = ok && gl_step<PROF, FAST>(o.c, h2, coarse_noise_gl_e<FAST>(xi0, xi1, e0, s0, s1, sc, bad),
-                                     m, ec, bad);
+      const double xic = coarse_noise_gl_e<FAST>(xi0, xi1, e0, s0, s1, sc, bad);
+      if (FIRST) {
+        double sd;
+        ou_terms<FAST>(cx0.lam, h2, ec, sd, bad);
+        ok = ok && gl_update<FAST>(o.c, cx0, h2, xic, ec, sd, m, bad);
+      } else {
+        ok = ok && gl_step<PROF, FAST>(o.c, h2, xic, m, ec, bad);
+      }
     } else {
       const double e = ou_decay<FAST>(cf.lam, h, bad);  // lam_fine at the window start
       int pm0, pm1, pmc;
@@ -120,6 +146,18 @@ __device__ __forceinline__ PathOut run_sample(const KernelArgs& a, uint64_t idx,
                                         coarse_noise_gl_e<FAST>(xi0, xi1, e, s0, s1, 1, bad),
                                         signs, pmc, m, bad);
     }
+    return ok;
+  };
+  const int64_t windows = a.M >> 1;
+  if (IG != kBAOAB && windows == 1) {
+    // level 1 (M = 2, the coupled level with the most samples): one window,
+    // both legs at x0.  (Peeling window 0 in front of the loop for every
+    // level instead costs the SE loop ~200 B of spills.)
+    o.ok = window(std::true_type{}, 0);
+    return o;
+  }
+  for (int64_t n = 0; n < windows; ++n) {
+    const bool ok = window(std::false_type{}, n);
     if (!ok) o.ok = false;
     if (!ok || (FAST && bad)) break;
   }

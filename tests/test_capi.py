@@ -281,3 +281,43 @@ def test_smoothing_polynomial_product_vs_goldens_and_criterion_9():
     assert worst <= 1e-10
     with pytest.raises(ValueError, match="r must be"):
         ablmc.build_smoothing_polynomial(13)
+
+
+def test_release_coeffs_equal_the_oracle_bit_for_bit():
+    """The samplers take every path's first-step sde_coeffs(x0) from the host
+    (capi.cu host_coeffs); they must be the reference's IEEE values bit for
+    bit (model.hpp:73-89; extension profiles as restated by the oracle), for
+    release heights inside, on the clamp boundaries, on the walls and outside
+    the layer, and for non-power-of-two H."""
+    import oracle_lib as O
+    lib = capi.load()
+    rng = np.random.default_rng(7)
+    out = (C.c_double * 4)()
+    cases = 0
+    for trial in range(400):
+        H = float(rng.choice([1.0, 2.0, 3.0, 0.75]))
+        mp = ablmc.ModelParams(kappa_sigma=float(rng.uniform(0.8, 2.0)),
+                               kappa_tau=float(rng.uniform(0.3, 0.9)),
+                               u_star=float(rng.choice([0.1, 0.2, 1e-12])), H=H,
+                               eps_reg=float(rng.choice([0.005, 0.01, 0.05])) * H, x_ref=H,
+                               noise_scale=float(rng.choice([1.0, 0.5])))
+        prof = ablmc.Profile(int(rng.integers(0, 3)))
+        kw = dict(const_sigma_u=1.3, const_tau=float(rng.choice([0.1, 0.5])), sigma_floor=1e-3,
+                  tau_min=1e-3, tau_max=1.0) if prof != ablmc.Profile.reference else {}
+        x0 = float(rng.choice([rng.uniform(0, 1), 0.0, 1.0, mp.eps_reg / H, 1 - mp.eps_reg / H,
+                               1.5, -0.01])) * H
+        pr = ablmc.Problem.make(mp, ablmc.Integrator.gl, ablmc.QoISpec(), x0, 0.1, 1.0, 4, 1,
+                                profile=prof, **kw)
+        assert lib.ablmc_release_coeffs(C.byref(pr._c), out) == 0
+        c = pr._c
+        O.orc().orc_set_profile(c.profile, c.const_sigma_u, c.const_tau, c.sigma_floor,
+                                c.tau_min, c.tau_max)
+        try:
+            ref = O.orc().orc_sde_coeffs(x0, C.byref(c.params))
+        finally:
+            O.orc().orc_set_profile(0, 0, 0, 0, 0, 0)
+        got = list(out)
+        want = [ref.sigma_u2, ref.lambda_, ref.sigma, ref.dsigma_u2]
+        assert np.array(got).tobytes() == np.array(want).tobytes(), (trial, prof, x0, got, want)
+        cases += 1
+    assert cases == 400

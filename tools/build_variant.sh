@@ -11,7 +11,7 @@ csrc="$ROOT/paper_1612_07717_b200/csrc"
 obj="$ROOT/paper_1612_07717_b200/build"
 out="$ROOT/paper_1612_07717_b200/variants"
 mkdir -p "$out"
-NV="nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -I$ROOT/include"
+NV="nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-ffp-contract=off -I$ROOT/include"
 $NV "$@" -Xptxas -v -c "$csrc/level_kernels.cu" -o "/tmp/lk_$name.o" 2>"/tmp/ptx_$name.txt"
 $NV "$@" -Xptxas -v -c "$csrc/adaptive_kernels.cu" -o "/tmp/ak_$name.o" 2>>"/tmp/ptx_$name.txt"
 $NV "$@" -c "$csrc/binned_kernels.cu" -o "/tmp/bk_$name.o"
