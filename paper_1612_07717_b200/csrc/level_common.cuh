@@ -250,6 +250,41 @@ __device__ __forceinline__ long long ordered_sum(const long long* p, int64_t n, 
   return v;
 }
 
+// Super-block order: the block partials of a super-block are folded in
+// segments of kSeg consecutive blocks (each segment a left fold from 0 in
+// block order), and the segment sums are folded in segment order.  One warp
+// computes the 32 segments in parallel (merge_tail_warp: ~2 load round trips
+// instead of 64 on the launch's tail); one thread per column computes the
+// same association sequentially (merge_tail, K4).
+constexpr int kSeg = 32;
+template <class T>
+__device__ __forceinline__ T seg_fold(const T* p, int64_t n, int64_t stride) {
+  T v = T(0);
+  for (int64_t s0 = 0; s0 < n; s0 += kSeg) {
+    const T seg = ordered_sum(p + s0 * stride, min(int64_t(kSeg), n - s0), stride);
+    if constexpr (std::is_floating_point<T>::value) v = add(v, seg);
+    else v += seg;
+  }
+  return v;
+}
+// the same value computed by one warp (all lanes return it)
+template <class T>
+__device__ __forceinline__ T seg_fold_warp(const T* p, int64_t n, int64_t stride) {
+  const int lane = threadIdx.x & 31;
+  const int64_t s0 = int64_t(lane) * kSeg;
+  T seg = T(0);
+  if (s0 < n) seg = ordered_sum(p + s0 * stride, min(int64_t(kSeg), n - s0), stride);
+  T v = T(0);
+  const int nseg = int((n + kSeg - 1) / kSeg);  // <= 32 (n <= ABLMC_BLOCKS_PER_SUPER)
+  for (int l = 0; l < nseg; ++l) {
+    const T x = __shfl_sync(0xffffffffu, seg, l);
+    if constexpr (std::is_floating_point<T>::value) v = add(v, x);
+    else v += x;
+  }
+  return v;
+}
+static_assert(ABLMC_BLOCKS_PER_SUPER <= 32 * kSeg, "one warp covers a super-block");
+
 // Per-CTA arrival counter of the tile epilogue (one per CTA; tile_prologue
 // zeroes it before any warp can arrive).
 __device__ __forceinline__ unsigned& tile_arrivals() {
@@ -265,7 +300,8 @@ __device__ __forceinline__ void tile_prologue() {
 // to finish in its CTA) for scalar QoIs (dim2 + kCnt <= 32 values): the last
 // tile of a 4096-sample block (arrival counter) sums the block's tile partials
 // in tile order, the last block of a 2^22-sample super-block sums the block
-// partials in block order -- the fixed sequential orders of merge_tail below.
+// partials in the segment order of seg_fold -- the fixed orders of merge_tail
+// below.
 __device__ __forceinline__ void merge_tail_warp(const KernelArgs& a, const double* tile_sums,
                                                 const long long* tile_cnt, int dim2) {
   const int lane = threadIdx.x & 31;
@@ -300,10 +336,14 @@ __device__ __forceinline__ void merge_tail_warp(const KernelArgs& a, const doubl
   if (!__shfl_sync(0xffffffffu, last, 0)) return;
   __threadfence();
   const int64_t so = a.sb_out + sb;
-  if (c < dim2) {
-    a.sb_sums[so * dim2 + c] = ordered_sum(a.blk_sums + b0 * dim2 + c, b1 - b0, dim2);
-  } else if (c < dim2 + kCnt) {
-    a.sb_cnt[kCnt * so + (c - dim2)] = ordered_sum(a.blk_cnt + kCnt * b0 + (c - dim2), b1 - b0, kCnt);
+  for (int k = 0; k < dim2 + kCnt; ++k) {  // the whole warp per column
+    if (k < dim2) {
+      const double v = seg_fold_warp(a.blk_sums + b0 * dim2 + k, b1 - b0, int64_t(dim2));
+      if (lane == 0) a.sb_sums[so * dim2 + k] = v;
+    } else {
+      const long long v = seg_fold_warp(a.blk_cnt + kCnt * b0 + (k - dim2), b1 - b0, int64_t(kCnt));
+      if (lane == 0) a.sb_cnt[kCnt * so + (k - dim2)] = v;
+    }
   }
   if (lane == 0) a.arr_sb[sb] = 0u;
 }
@@ -389,7 +429,7 @@ __device__ __forceinline__ void tile_reduce(const KernelArgs& a, bool active, bo
 // Single-pass merge, run by every CTA after its tile partial is written:
 // the last CTA of a 4096-sample block (arrival counter) sums the block's
 // tile partials in tile order, and the last block of a super-block sums the
-// block partials in block order -- the same fixed sequential orders as a
+// block partials in the segment order of seg_fold -- the same fixed orders as a
 // separate tile->block->super-block reduction, without two extra launches.
 // Counters reset themselves for the next launch.
 // `writers`: threads [0, writers) wrote this CTA's tile partial; only they
@@ -427,8 +467,8 @@ __device__ __forceinline__ void merge_tail(const KernelArgs& a, const double* ti
   __threadfence();
   const int64_t so = a.sb_out + sb;
   for (int c = threadIdx.x; c < dim2 + kCnt; c += blockDim.x) {
-    if (c < dim2) a.sb_sums[so * dim2 + c] = ordered_sum(a.blk_sums + b0 * dim2 + c, b1 - b0, dim2);
-    else a.sb_cnt[kCnt * so + (c - dim2)] = ordered_sum(a.blk_cnt + kCnt * b0 + (c - dim2), b1 - b0, kCnt);
+    if (c < dim2) a.sb_sums[so * dim2 + c] = seg_fold(a.blk_sums + b0 * dim2 + c, b1 - b0, int64_t(dim2));
+    else a.sb_cnt[kCnt * so + (c - dim2)] = seg_fold(a.blk_cnt + kCnt * b0 + (c - dim2), b1 - b0, int64_t(kCnt));
   }
   if (threadIdx.x == 0) a.arr_sb[sb] = 0u;
 }
