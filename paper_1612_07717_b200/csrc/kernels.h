@@ -28,11 +28,26 @@ constexpr int kCnt = 3;
 #define ABLMC_MINB_BAOAB 3
 #endif
 
+// The sample-independent part of a leg's first step from the release state
+// (x0, u0) with step h (capi.cu first_step; the device finishes it with the
+// sample's normal xi):
+//   SE:    u1 = AB + G xi               (AB = (1 - lam h) u0 - dv_dx(u0) h, G = sigma sqrt(h))
+//   GL:    u* = D + G xi                (D = e u0, G = sigma sd(lam, h))
+//   BAOAB: (x, u, par, nrefl) after the first B and A half-steps and the
+//          reflection, then u* = D + G xi' (D = decay u, G = sigma_mid sd_mid).
+struct FirstStep {
+  double AB, D, G, e;  // e: exp(-lam(x0) h) (GL/BAOAB coarse-noise weight)
+  double x, u;
+  int par, nrefl;
+};
+
 // Everything one launch needs, passed by value (kernel-parameter constant bank).
 struct KernelArgs {
   ablmc_dev::DevModel model;
   double x0, u0;
   ablmc_dev::Coef c_x0;     // sde_coeffs(x0): every sample's first-step coefficients (host)
+  FirstStep fs[2];          // first fine (h) / coarse (2h) step from (x0, u0), if fs_ok
+  int fs_ok;                // 1: fs valid (fixed u0, nothing exceptional in the first step)
   double h, sqrt_h;         // fine step T/M and sqrt(h)
   double h2, sqrt_h2;       // coarse step 2h and sqrt(2h)
   double h_half, h2_half;   // 0.5*h, 0.5*(2h) (BAOAB half steps)

@@ -23,6 +23,33 @@ struct PathOut {
   bool ok;
 };
 
+// A leg's first step from the release state, finished from its hoisted
+// sample-independent part F (KernelArgs::FirstStep, computed on the host with
+// this path's IEEE semantics) and the sample's normal xi: the same operations
+// on the same values as se_step / gl_step / baoab_step from (x0, u0).  h: the
+// step, hh = h/2 (BAOAB), scale: BAOAB's scale_noise_by_parity; BAOAB leaves
+// sde_coeffs at the new x in cend.
+template <int IG, int PROF, int FAST>
+__device__ __forceinline__ bool first_step_finish(PState& s, const FirstStep& F, const Coef& cx0,
+                                                  double h, double hh, double xi, bool scale,
+                                                  Coef& cend, const DevModel& m, bool& bad) {
+  if (IG == kSE) {
+    const double u1 = add(F.AB, mul(F.G, xi));
+    return reflect_t<FAST>(s, add(s.x, mul(u1, h)), u1, m, bad);
+  }
+  if (IG == kGL) {
+    const double us = add(F.D, mul(F.G, xi));
+    const double u1 = sub(us, mul(dv_dx<FAST>(cx0, us, bad), h));
+    return reflect_t<FAST>(s, add(s.x, mul(u1, h)), u1, m, bad);
+  }
+  s = {F.x, F.u, F.par, F.nrefl};
+  const double us = add(F.D, mul(F.G, scale ? sgn(s.par, xi) : xi));
+  if (!reflect_t<FAST>(s, add(s.x, mul(us, hh)), us, m, bad)) return false;
+  cend = coeffs<PROF, FAST>(s.x, m, bad);
+  s.u = sub(s.u, mul(dv_dx<FAST>(cend, s.u, bad), hh));
+  return true;
+}
+
 // simulate_pair (coupling.hpp:64-105) / simulate_path (coupling.hpp:22-29)
 // for one sample.  XI: read normals from xi (oracle mode) instead of Philox.
 // FAST: fast div/sqrt; returns early with bad = true on any fast-path miss
@@ -81,7 +108,20 @@ __device__ __forceinline__ PathOut run_sample(const KernelArgs& a, uint64_t idx,
       }
     };
     if (a.M <= 0) return o;
-    bool ok = step(std::true_type{}, 0);  // step 0 peeled (BAOAB: no difference)
+    bool ok;
+    if (a.fs_ok) {  // step 0 from its hoisted sample-independent part
+      double xi_0;
+      if (XI) {
+        xi_0 = xi[0];
+      } else {
+        normal_pair(0, idx, a.key, z0, z1);
+        xi_0 = z0;
+      }
+      ok = first_step_finish<IG, PROF, FAST>(o.f, a.fs[0], cx0, h, a.h_half, xi_0, false, c0, m,
+                                             bad);
+    } else {
+      ok = step(std::true_type{}, 0);  // step 0 peeled (BAOAB: no difference)
+    }
     for (int64_t k = 1; ok && !(FAST && bad) && k < a.M; ++k) ok = step(std::false_type{}, k);
     o.ok = ok;
     return o;
@@ -149,6 +189,49 @@ __device__ __forceinline__ PathOut run_sample(const KernelArgs& a, uint64_t idx,
     return ok;
   };
   const int64_t windows = a.M >> 1;
+  if (windows == 1 && a.fs_ok) {
+    // level 1 (M = 2, the coupled level with the most samples): one window;
+    // fine step 0 and the coarse step start at (x0, u0): their
+    // sample-independent parts come from the host (first_step_finish)
+    double xi0, xi1;
+    if (XI) {
+      xi0 = xi[0];
+      xi1 = xi[1];
+    } else {
+      normal_pair(0, idx, a.key, xi0, xi1);
+    }
+    const int p0 = o.f.par;
+    Coef cend;
+    bool ok = first_step_finish<IG, PROF, FAST>(o.f, a.fs[0], cx0, h, a.h_half, xi0, false, cend,
+                                                m, bad);
+    if (IG == kBAOAB) {
+      const int pm0 = a.fs[0].par;  // parity at the fine step-0 noise (after its first half)
+      int pm1, pmc;
+      Coef cfe = cend;
+      ok = ok && baoab_step<PROF, FAST>(o.f, cfe, h, a.h_half, xi1, false, pm1, m, bad);
+      const int s0 = signs ? pm0 : 1, s1 = signs ? pm1 : 1;
+      (void)pmc;
+      ok = ok && first_step_finish<IG, PROF, FAST>(
+                     o.c, a.fs[1], cx0, h2, a.h2_half,
+                     coarse_noise_gl_e<FAST>(xi0, xi1, a.fs[0].e, s0, s1, 1, bad), signs, cend, m,
+                     bad);
+    } else {
+      const int p1 = o.f.par;
+      if (IG == kSE) {
+        ok = ok && se_step<PROF, FAST>(o.f, h, sqrt_h, xi1, m, bad);
+      } else {
+        double e1;
+        ok = ok && gl_step<PROF, FAST>(o.f, h, xi1, m, e1, bad);
+      }
+      const int s0 = signs ? p0 : 1, s1 = signs ? p1 : 1, sc = signs ? o.c.par : 1;
+      const double xic = IG == kSE ? coarse_noise_se<FAST>(xi0, xi1, s0, s1, sc, bad)
+                                   : coarse_noise_gl_e<FAST>(xi0, xi1, a.fs[0].e, s0, s1, sc, bad);
+      ok = ok && first_step_finish<IG, PROF, FAST>(o.c, a.fs[1], cx0, h2, a.h2_half, xic, false,
+                                                   cend, m, bad);
+    }
+    o.ok = ok;
+    return o;
+  }
   if (IG != kBAOAB && windows == 1) {
     // level 1 (M = 2, the coupled level with the most samples): one window,
     // both legs at x0.  (Peeling window 0 in front of the loop for every

@@ -581,3 +581,47 @@ def test_degenerate_release_states_like_the_reference(x0, u0):
                 ig, level)
             if st.n:
                 assert close(acc.sum_y, st.sum_y, 1e-11, 1e-13)
+
+
+@pytest.mark.parametrize("ig", list(Ig))
+@pytest.mark.parametrize("prof", ["reference", "floored"])
+def test_first_steps_hoisted_bit_exact_given_device_math(ig, prof):
+    """Level 0 paths (M = 1..3) and level-1 pairs (M = 2) take their first
+    step's sample-independent part from the host (KernelArgs::FirstStep,
+    capi.cu first_step): device == oracle on the device's elementary
+    functions, bit for bit, over releases inside, near and on the walls, with
+    first half-steps that reflect (BAOAB), u0 = 0, signs on and off."""
+    kw = {}
+    if prof == "floored":
+        kw = dict(profile=ablmc.Profile.floored, sigma_floor=1e-3, tau_min=1e-3, tau_max=1.0)
+    O.orc().orc_set_device_math(1)
+    try:
+        for x0, u0, T in [(0.5, 0.1, 1.0), (0.02, -0.3, 1.0), (0.97, 0.4, 2.0), (0.0, -0.2, 1.0),
+                          (1.0, 0.3, 1.0), (0.3, 0.0, 0.5), (0.01, -1.5, 1.0)]:
+            for signs in (True, False):
+                pr = ablmc.Problem.make(ablmc.ModelParams(), ig, ablmc.QoISpec(), x0, u0, T, 1, 5,
+                                        ablmc.SampleOptions(signs_on=signs), **kw)
+                c = pr._c
+                O.orc().orc_set_profile(c.profile, c.const_sigma_u, c.const_tau, c.sigma_floor,
+                                        c.tau_min, c.tau_max)
+                got = ablmc.simulate_pairs(pr, 1, 1000, 64)
+                for i in range(64):
+                    rc, f, cc = O.orc_pair(int(ig), c.params, x0, u0, T, 2, 5, 1, 1000 + i,
+                                           signs_on=int(signs))
+                    assert (rc == 0) == bool(got["fok"][i]), (x0, u0, i)
+                    if rc == 0:
+                        assert [got["fx"][i], got["fu"][i], got["fpar"][i], got["fn"][i],
+                                got["cx"][i], got["cu"][i], got["cpar"][i], got["cn"][i]] == [
+                            f.x, f.u, f.parity, f.n_refl, cc.x, cc.u, cc.parity, cc.n_refl], (
+                            x0, u0, signs, i)
+                for M in (1, 2, 3):
+                    gp = ablmc.simulate_paths(pr, M, 77, 64, 0)
+                    for i in range(64):
+                        rc, s = O.orc_path(int(ig), c.params, x0, u0, T, M, 5, 0, 77 + i)
+                        assert (rc == 0) == bool(gp["ok"][i]), (x0, u0, M, i)
+                        if rc == 0:
+                            assert [gp["x"][i], gp["u"][i], gp["parity"][i], gp["n_refl"][i]] == [
+                                s.x, s.u, s.parity, s.n_refl], (x0, u0, M, i)
+    finally:
+        O.orc().orc_set_device_math(0)
+        O.orc().orc_set_profile(0, 0, 0, 0, 0, 0)
