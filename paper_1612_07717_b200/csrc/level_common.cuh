@@ -189,10 +189,13 @@ __device__ __forceinline__ PathOut run_sample(const KernelArgs& a, uint64_t idx,
     return ok;
   };
   const int64_t windows = a.M >> 1;
-  if (windows == 1 && a.fs_ok) {
-    // level 1 (M = 2, the coupled level with the most samples): one window;
-    // fine step 0 and the coarse step start at (x0, u0): their
-    // sample-independent parts come from the host (first_step_finish)
+  // Window 0 with both legs' first steps from the host (first_step_finish).
+  // Used for level 1 (one window) and, reference profile GL/BAOAB, levels 2-3
+  // (the coupled levels with the most samples).  Higher levels keep the
+  // single-body loop: there the hoisting is worth < 2%, and a window peeled
+  // in front of the SE loop -- or of the extension profiles' loops -- costs
+  // them spills.
+  auto window0_hoisted = [&]() -> bool {
     double xi0, xi1;
     if (XI) {
       xi0 = xi[0];
@@ -206,14 +209,13 @@ __device__ __forceinline__ PathOut run_sample(const KernelArgs& a, uint64_t idx,
                                                 m, bad);
     if (IG == kBAOAB) {
       const int pm0 = a.fs[0].par;  // parity at the fine step-0 noise (after its first half)
-      int pm1, pmc;
-      Coef cfe = cend;
-      ok = ok && baoab_step<PROF, FAST>(o.f, cfe, h, a.h_half, xi1, false, pm1, m, bad);
+      int pm1;
+      cf = cend;
+      ok = ok && baoab_step<PROF, FAST>(o.f, cf, h, a.h_half, xi1, false, pm1, m, bad);
       const int s0 = signs ? pm0 : 1, s1 = signs ? pm1 : 1;
-      (void)pmc;
       ok = ok && first_step_finish<IG, PROF, FAST>(
                      o.c, a.fs[1], cx0, h2, a.h2_half,
-                     coarse_noise_gl_e<FAST>(xi0, xi1, a.fs[0].e, s0, s1, 1, bad), signs, cend, m,
+                     coarse_noise_gl_e<FAST>(xi0, xi1, a.fs[0].e, s0, s1, 1, bad), signs, cc, m,
                      bad);
     } else {
       const int p1 = o.f.par;
@@ -229,6 +231,16 @@ __device__ __forceinline__ PathOut run_sample(const KernelArgs& a, uint64_t idx,
       ok = ok && first_step_finish<IG, PROF, FAST>(o.c, a.fs[1], cx0, h2, a.h2_half, xic, false,
                                                    cend, m, bad);
     }
+    return ok;
+  };
+  constexpr bool kPeelMore = IG != kSE && PROF == kProfileReference;
+  if (a.fs_ok && windows == 1) {  // level 1: the whole sample
+    o.ok = window0_hoisted();
+    return o;
+  }
+  if (kPeelMore && a.fs_ok && windows <= 4) {  // levels 2-3
+    bool ok = window0_hoisted();
+    for (int64_t n = 1; ok && !(FAST && bad) && n < windows; ++n) ok = window(std::false_type{}, n);
     o.ok = ok;
     return o;
   }

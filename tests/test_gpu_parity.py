@@ -586,7 +586,7 @@ def test_degenerate_release_states_like_the_reference(x0, u0):
 @pytest.mark.parametrize("ig", list(Ig))
 @pytest.mark.parametrize("prof", ["reference", "floored"])
 def test_first_steps_hoisted_bit_exact_given_device_math(ig, prof):
-    """Level 0 paths (M = 1..3) and level-1 pairs (M = 2) take their first
+    """Level 0 paths (M = 1..3) and level 1-3 pairs (M = 2..8) take their first
     step's sample-independent part from the host (KernelArgs::FirstStep,
     capi.cu first_step): device == oracle on the device's elementary
     functions, bit for bit, over releases inside, near and on the walls, with
@@ -604,16 +604,17 @@ def test_first_steps_hoisted_bit_exact_given_device_math(ig, prof):
                 c = pr._c
                 O.orc().orc_set_profile(c.profile, c.const_sigma_u, c.const_tau, c.sigma_floor,
                                         c.tau_min, c.tau_max)
-                got = ablmc.simulate_pairs(pr, 1, 1000, 64)
-                for i in range(64):
-                    rc, f, cc = O.orc_pair(int(ig), c.params, x0, u0, T, 2, 5, 1, 1000 + i,
-                                           signs_on=int(signs))
-                    assert (rc == 0) == bool(got["fok"][i]), (x0, u0, i)
-                    if rc == 0:
-                        assert [got["fx"][i], got["fu"][i], got["fpar"][i], got["fn"][i],
-                                got["cx"][i], got["cu"][i], got["cpar"][i], got["cn"][i]] == [
-                            f.x, f.u, f.parity, f.n_refl, cc.x, cc.u, cc.parity, cc.n_refl], (
-                            x0, u0, signs, i)
+                for level in (1, 2, 3):
+                    got = ablmc.simulate_pairs(pr, level, 1000, 64)
+                    for i in range(64):
+                        rc, f, cc = O.orc_pair(int(ig), c.params, x0, u0, T, 1 << level, 5, level,
+                                               1000 + i, signs_on=int(signs))
+                        assert (rc == 0) == bool(got["fok"][i]), (x0, u0, level, i)
+                        if rc == 0:
+                            assert [got["fx"][i], got["fu"][i], got["fpar"][i], got["fn"][i],
+                                    got["cx"][i], got["cu"][i], got["cpar"][i], got["cn"][i]] == [
+                                f.x, f.u, f.parity, f.n_refl, cc.x, cc.u, cc.parity, cc.n_refl], (
+                                x0, u0, signs, level, i)
                 for M in (1, 2, 3):
                     gp = ablmc.simulate_paths(pr, M, 77, 64, 0)
                     for i in range(64):
