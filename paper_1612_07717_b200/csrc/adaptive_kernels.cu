@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cstddef>
+#include <type_traits>
 
 #include "level_common.cuh"
 
@@ -135,7 +136,17 @@ __device__ __forceinline__ double backward_sum(int n, Term term, Decay decay) {
 }
 
 struct PendLocal {
+  static constexpr int kCap = kPendLocal;
   double t[kPendLocal], e[kPendLocal];
+};
+// K1D: the same terms in global memory (a per-thread slice of ad_scratch),
+// for the rare pairs whose legs exceed kPendLocal; beyond kPendDeep the
+// Horner form is the last resort.
+constexpr int kPendDeep = ABLMC_PEND_DEEP;
+struct PendGlobal {
+  static constexpr int kCap = kPendDeep;
+  double* t;
+  double* e;
 };
 
 // coupling.hpp:140-155
@@ -157,18 +168,20 @@ __device__ __forceinline__ void leg_schedule(ALeg& L, double base, double T, dou
 // reference does.  GL/BAOAB: the term S xi sd(lam, dt) and weight
 // exp(-lam dt) are stored for the backward sum at the step (leg_settle);
 // the Horner form acc <- acc e + term is kept alongside for overflow.
-template <int IG, int FAST>
-__device__ __forceinline__ void leg_push(ALeg& L, PendLocal& P, double xi_s, double dt,
-                                         double sqrt_dt, bool& bad) {
+template <int IG, int FAST, class Pend>
+__device__ __forceinline__ void leg_push(ALeg& L, Pend& P, double xi_s, double dt,
+                                         double sqrt_dt, bool& bad, bool& deep) {
   if (IG == kSE) {
     L.acc = add(L.acc, mul(xi_s, sqrt_dt));
   } else {
     double e, sd;
     ou_terms<FAST>(L.c.lam, dt, e, sd, bad);
     const double term = mul(xi_s, sd);
-    if (L.np < kPendLocal) {
+    if (L.np < Pend::kCap) {
       P.t[L.np] = term;
       P.e[L.np] = e;
+    } else {
+      deep = true;
     }
     ++L.np;
     L.acc = add(mul(L.acc, e), term);
@@ -176,9 +189,9 @@ __device__ __forceinline__ void leg_push(ALeg& L, PendLocal& P, double xi_s, dou
 }
 
 // the pending increment of a GL/BAOAB leg about to step (register version)
-template <int IG>
-__device__ __forceinline__ void leg_settle(ALeg& L, const PendLocal& P) {
-  if (IG != kSE && L.np >= 3 && L.np <= kPendLocal)  // <= 2: Horner == backward sum
+template <int IG, class Pend>
+__device__ __forceinline__ void leg_settle(ALeg& L, const Pend& P) {
+  if (IG != kSE && L.np >= 3 && L.np <= Pend::kCap)  // <= 2: Horner == backward sum
     L.acc = backward_sum(L.np, [&](int r) { return P.t[r]; }, [&](int r) { return P.e[r]; });
 }
 
@@ -213,9 +226,13 @@ __device__ __forceinline__ bool leg_take(ALeg& L, bool is_coarse, const DevModel
 }
 
 // coupling.hpp:137-214 — coupled pair on non-nested adaptive grids.
-template <int IG, int PROF, int FAST>
+// DEEP = false: pending terms in local memory; a leg that exceeds kPendLocal
+// sets `deep` and ends the sample (its result is discarded: K1D recomputes it
+// with DEEP = true and global-memory storage at `scratch`).
+template <int IG, int PROF, int FAST, bool DEEP = false>
 __device__ __forceinline__ PathOut run_pair_adaptive(const KernelArgs& a, uint64_t idx,
-                                                     long long& steps, bool& bad) {
+                                                     long long& steps, bool& bad, bool& deep,
+                                                     double* scratch = nullptr) {
   using O = Ops<FAST>;
   const DevModel& m = a.model;
   const double T = a.T, hb = a.h_base, hb2 = mul(2.0, a.h_base);
@@ -232,7 +249,13 @@ __device__ __forceinline__ PathOut run_pair_adaptive(const KernelArgs& a, uint64
   leg_schedule<FAST>(f, hb, T, lam_ref, bad);
   leg_schedule<FAST>(c, hb2, T, lam_ref, bad);
   SeqNoise<PhiloxKey> ns;
-  PendLocal pf, pc;
+  using Pend = typename std::conditional<DEEP, PendGlobal, PendLocal>::type;
+  Pend pf, pc;
+  if constexpr (DEEP) {
+    pf = {scratch, scratch + kPendDeep};
+    pc = {scratch + 2 * kPendDeep, scratch + 3 * kPendDeep};
+  }
+  (void)scratch;
   const bool signs = a.signs_on;
   PathOut o;
   o.ok = true;
@@ -246,8 +269,9 @@ __device__ __forceinline__ PathOut run_pair_adaptive(const KernelArgs& a, uint64
       const double xi = ns.next(idx, a.key);
       const double sqrt_dt = IG == kSE ? O::sqrt(dt, bad) : 0.0;
       const int sf = signs ? f.s.par : 1;
-      if (!f.done) leg_push<IG, FAST>(f, pf, xi, dt, sqrt_dt, bad);
-      if (!c.done) leg_push<IG, FAST>(c, pc, sgn(sf, xi), dt, sqrt_dt, bad);
+      if (!f.done) leg_push<IG, FAST>(f, pf, xi, dt, sqrt_dt, bad, deep);
+      if (!c.done) leg_push<IG, FAST>(c, pc, sgn(sf, xi), dt, sqrt_dt, bad, deep);
+      if (!DEEP && deep) break;
     }
     if (!f.done && f.t_next == tau) {
       leg_settle<IG>(f, pf);
@@ -273,24 +297,28 @@ __device__ __forceinline__ PathOut run_pair_adaptive(const KernelArgs& a, uint64
 
 template <int IG, int PROF, bool COUPLED, int FAST>
 __device__ __forceinline__ PathOut run_adaptive(const KernelArgs& a, uint64_t idx,
-                                                long long& steps, bool& bad) {
-  if (COUPLED) return run_pair_adaptive<IG, PROF, FAST>(a, idx, steps, bad);
+                                                long long& steps, bool& bad, bool& deep) {
+  if (COUPLED) return run_pair_adaptive<IG, PROF, FAST>(a, idx, steps, bad, deep);
   return run_path_adaptive<IG, PROF, FAST>(a, idx, steps, bad);
 }
 
 // Fast variant first when the host certified tame parameters; a miss
 // recomputes the sample exactly (same policy as sample()).
+// deep: a leg exceeded kPendLocal pending sub-intervals (result invalid; the
+// caller queues the sample for K1D).
 template <int IG, int PROF, bool COUPLED>
 __device__ __forceinline__ PathOut sample_adaptive(const KernelArgs& a, uint64_t idx,
-                                                   long long& steps) {
+                                                   long long& steps, bool& deep) {
   bool bad = false;
+  deep = false;
   if (a.fast) {
-    PathOut o = a.fast == kFastUnit ? run_adaptive<IG, PROF, COUPLED, kFastUnit>(a, idx, steps, bad)
-                                    : run_adaptive<IG, PROF, COUPLED, 1>(a, idx, steps, bad);
-    if (!bad) return o;
+    PathOut o = a.fast == kFastUnit
+                    ? run_adaptive<IG, PROF, COUPLED, kFastUnit>(a, idx, steps, bad, deep)
+                    : run_adaptive<IG, PROF, COUPLED, 1>(a, idx, steps, bad, deep);
+    if (!bad || deep) return o;
     bad = false;
   }
-  return run_adaptive<IG, PROF, COUPLED, 0>(a, idx, steps, bad);
+  return run_adaptive<IG, PROF, COUPLED, 0>(a, idx, steps, bad, deep);
 }
 
 // ----------------------------------------- persistent adaptive sampler
@@ -401,7 +429,8 @@ __device__ __forceinline__ ALeg leg_load(const LegStore& st, int leg, const LegH
 // terms go to shared memory (overflow: FAST recomputes the sample in K1R)
 template <int IG, int FAST>
 __device__ __forceinline__ void hot_push(LegHot& L, LegStore& st, PendSpill& sp, int leg,
-                                         double xi_s, double dt, double sqrt_dt, bool& bad) {
+                                         double xi_s, double dt, double sqrt_dt, bool& bad,
+                                         bool& deep) {
   if (IG == kSE) {
     L.acc = add(L.acc, mul(xi_s, sqrt_dt));
   } else {
@@ -414,8 +443,8 @@ __device__ __forceinline__ void hot_push(LegHot& L, LegStore& st, PendSpill& sp,
     } else if (L.np < kPendLocal) {
       sp.t[leg][L.np - kPend] = term;
       sp.e[leg][L.np - kPend] = e;
-    } else if (FAST) {
-      bad = true;
+    } else {
+      deep = true;  // the sample goes to K1D
     }
     ++L.np;
     L.acc = add(mul(L.acc, e), term);
@@ -427,7 +456,7 @@ __device__ __forceinline__ void hot_push(LegHot& L, LegStore& st, PendSpill& sp,
 template <int IG, int PROF, int FAST>
 __device__ __forceinline__ bool pair_event(PairSM& S, LegStore& st, PendSpill& sp,
                                            const KernelArgs& a, uint64_t idx, double lam_ref,
-                                           bool& ok, bool& bad) {
+                                           bool& ok, bool& bad, bool& deep) {
   using O = Ops<FAST>;
   const double T = a.T;
   bool take_fine;
@@ -439,8 +468,9 @@ __device__ __forceinline__ bool pair_event(PairSM& S, LegStore& st, PendSpill& s
       const double xi = S.ns.next(idx, a.key);
       const double sqrt_dt = IG == kSE ? O::sqrt(dt, bad) : 0.0;
       const int sf = a.signs_on ? S.f.par : 1;
-      if (!S.f.done) hot_push<IG, FAST>(S.f, st, sp, 0, xi, dt, sqrt_dt, bad);
-      if (!S.c.done) hot_push<IG, FAST>(S.c, st, sp, 1, sgn(sf, xi), dt, sqrt_dt, bad);
+      if (!S.f.done) hot_push<IG, FAST>(S.f, st, sp, 0, xi, dt, sqrt_dt, bad, deep);
+      if (!S.c.done) hot_push<IG, FAST>(S.c, st, sp, 1, sgn(sf, xi), dt, sqrt_dt, bad, deep);
+      if (deep) return true;
     }
     take_fine = !S.f.done && S.f.t_next == S.tau;
     S.pend_c = take_fine && !S.c.done && S.c.t_next == S.tau;
@@ -529,6 +559,7 @@ __global__ void __launch_bounds__(kTile, ABLMC_MINB_ADAPTIVE) k_adaptive_persist
     leg_schedule<FAST>(c0, mul(2.0, a.h_base), a.T, lam_ref, bad);
   }
   const bool bad0 = bad;
+  bool deep = false;
   extern __shared__ double4 ad_smem[];
   LegStore& st = *reinterpret_cast<LegStore*>(ad_smem);  // COUPLED only (dynamic size 0 else)
   PairSM P;
@@ -552,16 +583,19 @@ __global__ void __launch_bounds__(kTile, ABLMC_MINB_ADAPTIVE) k_adaptive_persist
       Q.ns.k = 0;
     }
     bad = bad0;
+    deep = false;
   };
   int64_t j = grab_sample(a.ad_ctrl);
   if (j < a.n) start();
   while (j < a.n) {
     const uint64_t idx = uint64_t(a.first + a.offset + j);
     bool ok = true;
-    const bool fin = COUPLED ? pair_event<IG, PROF, FAST>(P, st, sp, a, idx, lam_ref, ok, bad)
+    const bool fin = COUPLED ? pair_event<IG, PROF, FAST>(P, st, sp, a, idx, lam_ref, ok, bad, deep)
                              : path_event<IG, PROF, FAST>(Q, a, idx, lam_ref, ok, bad);
     if (fin) {
-      if (FAST && bad) {
+      if (deep) {
+        a.ad_deep[atomicAdd(a.ad_ctrl + 2, 1ull)] = j;
+      } else if (FAST && bad) {
         a.ad_redo[atomicAdd(a.ad_ctrl + 1, 1ull)] = j;
       } else {
         PathOut o;
@@ -592,11 +626,47 @@ __global__ void __launch_bounds__(kTile) k_adaptive_redo(const KernelArgs a) {
   for (int64_t r = int64_t(blockIdx.x) * kTile + threadIdx.x; r < nr;
        r += int64_t(gridDim.x) * kTile) {
     const int64_t j = a.ad_redo[r];
-    bool bad = false;
+    bool bad = false, deep = false;
     long long steps = 0;
     const PathOut o = run_adaptive<IG, PROF, COUPLED, 0>(a, uint64_t(a.first + a.offset + j),
-                                                         steps, bad);
-    adaptive_store<COUPLED>(a, j, o, steps);
+                                                         steps, bad, deep);
+    if (deep) a.ad_deep[atomicAdd(a.ad_ctrl + 2, 1ull)] = j;
+    else adaptive_store<COUPLED>(a, j, o, steps);
+  }
+}
+
+__device__ __forceinline__ StateOut state_out(const PathOut& o, long long steps) {
+  StateOut s;
+  s.fx = o.f.x;
+  s.fu = o.f.u;
+  s.fpar = o.f.par;
+  s.fn = o.f.nrefl;
+  s.cx = o.c.x;
+  s.cu = o.c.u;
+  s.cpar = o.c.par;
+  s.cn = o.c.nrefl;
+  s.ok = o.ok ? 1 : 0;
+  s.steps = int(steps);
+  return s;
+}
+
+// K1D: the pairs with more than kPendLocal pending sub-intervals on a leg,
+// recomputed exactly with their pending terms in global memory (a slice of
+// ad_scratch per thread; ABLMC_DEEP_THREADS threads stride over the list).
+// STATES: write the oracle-mode record instead of the per-sample slots.
+template <int IG, int PROF, bool STATES>
+__global__ void __launch_bounds__(64) k_adaptive_deep(const KernelArgs a, StateOut* __restrict__ out) {
+  const int64_t nd = int64_t(a.ad_ctrl[2]);
+  const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  double* scratch = a.ad_scratch + tid * 4 * kPendDeep;
+  for (int64_t r = tid; r < nd; r += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t j = a.ad_deep[r];
+    bool bad = false, deep = false;
+    long long steps = 0;
+    const PathOut o = run_pair_adaptive<IG, PROF, 0, true>(a, uint64_t(a.first + a.offset + j),
+                                                           steps, bad, deep, scratch);
+    if (STATES) out[j] = state_out(o, steps);
+    else adaptive_store<true>(a, j, o, steps);
   }
 }
 
@@ -617,7 +687,7 @@ __global__ void __launch_bounds__(kTile) k_adaptive_tiles(const KernelArgs a,
 template <int IG, int PROF, bool COUPLED>
 cudaError_t launch_adaptive(const KernelArgs& a, double* tile_sums, long long* tile_cnt,
                             cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(a.ad_ctrl, 0, 2 * sizeof(unsigned long long), st);
+  cudaError_t e = cudaMemsetAsync(a.ad_ctrl, 0, 3 * sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
@@ -640,6 +710,10 @@ cudaError_t launch_adaptive(const KernelArgs& a, double* tile_sums, long long* t
     k_adaptive_redo<IG, PROF, COUPLED><<<unsigned(sms), kTile, 0, st>>>(a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
+  if (COUPLED && IG != kSE) {  // K1D (exits at once when no pair went deep)
+    k_adaptive_deep<IG, PROF, false><<<ABLMC_DEEP_THREADS / 64, 64, 0, st>>>(a, nullptr);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
   k_adaptive_tiles<<<unsigned(tiles), kTile, 0, st>>>(a, tile_sums, tile_cnt);
   return cudaGetLastError();
 }
@@ -650,19 +724,11 @@ __global__ void __launch_bounds__(kTile) k_states_adaptive(const KernelArgs a,
   const int64_t j = int64_t(blockIdx.x) * kTile + threadIdx.x;
   if (j >= a.n) return;
   long long steps = 0;
-  const PathOut o = sample_adaptive<IG, PROF, COUPLED>(a, uint64_t(a.first + a.offset + j), steps);
-  StateOut s;
-  s.fx = o.f.x;
-  s.fu = o.f.u;
-  s.fpar = o.f.par;
-  s.fn = o.f.nrefl;
-  s.cx = o.c.x;
-  s.cu = o.c.u;
-  s.cpar = o.c.par;
-  s.cn = o.c.nrefl;
-  s.ok = o.ok ? 1 : 0;
-  s.steps = int(steps);
-  out[j] = s;
+  bool deep;
+  const PathOut o =
+      sample_adaptive<IG, PROF, COUPLED>(a, uint64_t(a.first + a.offset + j), steps, deep);
+  if (deep) a.ad_deep[atomicAdd(a.ad_ctrl + 2, 1ull)] = j;  // K1D writes out[j]
+  else out[j] = state_out(o, steps);
 }
 
 template <int IG, int PROF>
@@ -674,8 +740,12 @@ cudaError_t level_t(const KernelArgs& a, bool coupled, double* ts, long long* tc
 template <int IG, int PROF>
 cudaError_t states_t(const KernelArgs& a, bool coupled, StateOut* out, cudaStream_t st) {
   const dim3 g{unsigned((a.n + kTile - 1) / kTile)};
+  cudaError_t e = cudaMemsetAsync(a.ad_ctrl, 0, 3 * sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return e;
   if (coupled) k_states_adaptive<IG, PROF, true><<<g, kTile, 0, st>>>(a, out);
   else k_states_adaptive<IG, PROF, false><<<g, kTile, 0, st>>>(a, out);
+  if ((e = cudaGetLastError()) != cudaSuccess || !coupled || IG == kSE) return e;
+  k_adaptive_deep<IG, PROF, true><<<ABLMC_DEEP_THREADS / 64, 64, 0, st>>>(a, out);
   return cudaGetLastError();
 }
 

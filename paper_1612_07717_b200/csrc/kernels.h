@@ -80,6 +80,10 @@ struct KernelArgs {
   long long* ad_steps;      // steps taken, -1 = failed sample
   unsigned long long* ad_ctrl;
   long long* ad_redo;       // samples whose fast path missed (recomputed exactly)
+  long long* ad_deep;       // GL/BAOAB pairs with > 64 pending sub-intervals on a leg
+                            // (K1D recomputes them with global-memory pending storage);
+                            // ad_ctrl = {next sample, redo count, deep count}
+  double* ad_scratch;       // K1D: per-thread pending storage, 4 * ABLMC_PEND_DEEP doubles
   // single-pass merge inside the sampler launch: tile -> 4096-sample block ->
   // super-block partials (merge_tail), arrival counters zero between launches
   double* blk_sums;
@@ -90,6 +94,10 @@ struct KernelArgs {
   unsigned* arr_sb;
   int64_t sb_out;           // super-block row of this launch's first super-block
 };
+
+// K1D geometry and per-thread pending capacity (adaptive_kernels.cu)
+#define ABLMC_PEND_DEEP 4096
+#define ABLMC_DEEP_THREADS (32 * 64)
 
 struct StateOut {
   double fx, fu, cx, cu;

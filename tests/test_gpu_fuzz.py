@@ -15,7 +15,7 @@ from paper_1612_07717_b200 import ablmc
 
 pytestmark = pytest.mark.gpu
 Ig = ablmc.Integrator
-KPEND_LOCAL = 64  # pending sub-intervals a device leg stores (adaptive_kernels.cu kPendLocal)
+KPEND_DEEP = 4096  # pending sub-intervals a device leg can store (adaptive_kernels.cu kPendDeep)
 
 
 def random_problem(rng):
@@ -70,12 +70,13 @@ def test_random_problems_bit_exact_given_device_math(trial):
                                        first + i, signs_on=c.signs_on)
             g = got[i]
             assert (rc == 0) == bool(g["fok"]), (trial, i)
-            # GL/BAOAB adaptive legs store up to 64 pending sub-intervals for
-            # the reference's backward sum; beyond that the device uses the
-            # Horner form (adaptive_kernels.cu), equal within rounding: such
-            # samples are held to the north-star 1e-12 instead of bit identity.
+            # GL/BAOAB adaptive legs store the pending sub-intervals for the
+            # reference's backward sum (64 in local memory, K1D: 4096 in
+            # global memory); beyond that the device uses the Horner form,
+            # equal within rounding: such samples are held to the north-star
+            # 1e-12 instead of bit identity.
             deep = (c.adaptive and c.integrator != Ig.se
-                    and O.orc().orc_last_max_pending() > KPEND_LOCAL)
+                    and O.orc().orc_last_max_pending() > KPEND_DEEP)
             if rc == 0 and deep:
                 assert [g["fpar"], g["fn"], g["cpar"], g["cn"]] == [
                     f.parity, f.n_refl, cc.parity, cc.n_refl], (trial, i)
@@ -88,3 +89,45 @@ def test_random_problems_bit_exact_given_device_math(trial):
     finally:
         O.orc().orc_set_device_math(0)
         O.orc().orc_set_profile(0, 0, 0, 0, 0, 0)
+
+
+def test_deep_pending_pairs_bit_exact():
+    """A problem whose adaptive GL/BAOAB pairs exceed the 64 pending
+    sub-intervals a leg keeps in local memory (fuzz trial 48: H = 3, release
+    near the ground, signs off): K1D recomputes them with global-memory
+    storage, so the states (pair_states) are bit-identical to the oracle and
+    the accumulate path (K1P -> K1D -> K1T) sums the same samples."""
+    import ctypes as C
+    for ig in (Ig.gl, Ig.baoab):
+        rng = np.random.default_rng(1000 + 48)
+        pr, level = random_problem(rng)
+        c = pr._c
+        c.integrator = int(ig)
+        first = int(rng.integers(0, 2**32))
+        n = 256
+        got = ablmc.simulate_pairs(pr, level, first, n)
+        M = c.m0 << level
+        O.orc().orc_set_device_math(1)
+        deep = 0
+        try:
+            for i in range(n):
+                rc, f, cc, _ = O.orc_pair_adaptive(c.integrator, c.params, c.x0, c.u0, c.T,
+                                                   c.T / M, c.x_adapt, c.seed, level, first + i,
+                                                   c.signs_on)
+                deep += O.orc().orc_last_max_pending() > 64
+                g = got[i]
+                assert (rc == 0) == bool(g["fok"]), (ig, i)
+                if rc == 0:
+                    assert [g["fx"], g["fu"], g["fpar"], g["fn"], g["cx"], g["cu"], g["cpar"],
+                            g["cn"]] == [f.x, f.u, f.parity, f.n_refl, cc.x, cc.u, cc.parity,
+                                         cc.n_refl], (ig, i)
+            acc = ablmc.LevelStats().init(level, pr.h_level(level), 1)
+            ablmc.accumulate_samples(acc, first, n, pr, level)
+            st = O.Stats(1)
+            assert O.orc().orc_accumulate_samples(C.byref(c), level, first, n,
+                                                  C.byref(st.c)) == 0
+            assert (acc.n, acc.failed, acc.cost_steps) == (st.n, st.failed, st.cost_steps)
+            assert abs(acc.sum_y[0] - st.sum_y[0]) <= 1e-12 * max(1.0, abs(st.sum_y[0]))
+        finally:
+            O.orc().orc_set_device_math(0)
+        assert deep > 0, ig  # the problem does exercise K1D
