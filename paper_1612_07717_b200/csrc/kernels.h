@@ -46,8 +46,6 @@ struct KernelArgs {
   ablmc_dev::DevModel model;
   double x0, u0;
   ablmc_dev::Coef c_x0;     // sde_coeffs(x0): every sample's first-step coefficients (host)
-  FirstStep fs[2];          // first fine (h) / coarse (2h) step from (x0, u0), if fs_ok
-  int fs_ok;                // 1: fs valid (fixed u0, nothing exceptional in the first step)
   double h, sqrt_h;         // fine step T/M and sqrt(h)
   double h2, sqrt_h2;       // coarse step 2h and sqrt(2h)
   double h_half, h2_half;   // 0.5*h, 0.5*(2h) (BAOAB half steps)
@@ -93,6 +91,10 @@ struct KernelArgs {
   unsigned* arr_blk;
   unsigned* arr_sb;
   int64_t sb_out;           // super-block row of this launch's first super-block
+  // (last: the hot fields above keep their parameter-bank offsets, which the
+  // level-10 loop's constant loads are scheduled around)
+  FirstStep fs[2];          // first fine (h) / coarse (2h) step from (x0, u0), if fs_ok
+  int fs_ok;                // 1: fs valid (fixed u0, nothing exceptional in the first step)
 };
 
 // K1D geometry and per-thread pending capacity (adaptive_kernels.cu)
