@@ -408,7 +408,19 @@ def run_b200(a):
     torch.cuda.set_device(local)
     dist_on = world > 1 or a.force_dist
     if dist_on:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # NCCL's own log lines ("NCCL version ..." with this image's
+        # NCCL_DEBUG=VERSION) go to stderr: stdout carries only the JSON line.
+        # device_id makes the communicator initialisation eager, inside here.
+        sys.stdout.flush()
+        saved = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.barrier()
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved, 1)
+            os.close(saved)
     ablmc.init(local)
     # A dedicated (non-default) stream shared by torch and the library, so the
     # CUDA events below bracket exactly the library's kernels.
