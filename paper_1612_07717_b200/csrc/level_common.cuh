@@ -15,6 +15,9 @@ namespace {
 
 using namespace ablmc_dev;
 
+#ifndef ABLMC_PEEL_WINDOWS
+#define ABLMC_PEEL_WINDOWS 16  // hoisted window 0 up to level 5 (GL/BAOAB, reference profile)
+#endif
 constexpr int kTile = ABLMC_TILE;            // samples per CTA (one per thread)
 constexpr int kWarps = kTile / 32;
 
@@ -190,7 +193,7 @@ __device__ __forceinline__ PathOut run_sample(const KernelArgs& a, uint64_t idx,
   };
   const int64_t windows = a.M >> 1;
   // Window 0 with both legs' first steps from the host (first_step_finish).
-  // Used for level 1 (one window) and, reference profile GL/BAOAB, levels 2-3
+  // Used for level 1 (one window) and, reference profile GL/BAOAB, levels 2-5
   // (the coupled levels with the most samples).  Higher levels keep the
   // single-body loop: there the hoisting is worth < 2%, and a window peeled
   // in front of the SE loop -- or of the extension profiles' loops -- costs
@@ -238,7 +241,7 @@ __device__ __forceinline__ PathOut run_sample(const KernelArgs& a, uint64_t idx,
     o.ok = window0_hoisted();
     return o;
   }
-  if (kPeelMore && a.fs_ok && windows <= 4) {  // levels 2-3
+  if (kPeelMore && a.fs_ok && windows <= ABLMC_PEEL_WINDOWS) {  // levels 2-5
     bool ok = window0_hoisted();
     for (int64_t n = 1; ok && !(FAST && bad) && n < windows; ++n) ok = window(std::false_type{}, n);
     o.ok = ok;
