@@ -321,3 +321,13 @@ def test_release_coeffs_equal_the_oracle_bit_for_bit():
         assert np.array(got).tobytes() == np.array(want).tobytes(), (trial, prof, x0, got, want)
         cases += 1
     assert cases == 400
+
+
+@pytest.mark.parametrize("x_adapt", [-0.05, -0.0, 0.0, 1.5])
+def test_adaptive_reference_height_validated(x_adapt):
+    """SampleOptions::x_adapt outside (0, H] is rejected when the problem is
+    built (the fast path may therefore assume x_adapt in the layer)."""
+    opt = ablmc.SampleOptions(adaptive=True, x_adapt=x_adapt)
+    with pytest.raises(ValueError, match="x_adapt"):
+        ablmc.Problem.make(ablmc.ModelParams(), ablmc.Integrator.gl, ablmc.QoISpec(), 0.3, 0.1,
+                           1.0, 8, 3, opt)

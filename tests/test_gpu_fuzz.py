@@ -131,3 +131,4 @@ def test_deep_pending_pairs_bit_exact():
         finally:
             O.orc().orc_set_device_math(0)
         assert deep > 0, ig  # the problem does exercise K1D
+
