@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target wall time of the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-step-seconds", type=float, default=None,
+                    help="reference arm: CPU seconds per step (default: ~60 s over the run)")
     ap.add_argument("--force-dist", action="store_true",
                     help="use the NCCL process group and collectives even at world size 1")
     ap.add_argument("--no-extras", action="store_true",
@@ -62,6 +64,38 @@ def problem_c(ig: int):
                               1.0, 1, SEED)
 
 
+class _RefProblem:
+    """The C5 problem descriptor for the reference arm, filled field by field
+    (the reference's defaults: model.hpp:29-35, qoi.hpp:108-112,
+    estimators.hpp:27-36, coupling.hpp:218-220) WITHOUT the product library:
+    the reference arm must not map libablmc_b200.so."""
+
+    def __init__(self, ig: int):
+        from paper_1612_07717_b200 import capi  # ctypes structs only; loads nothing
+        c = capi.ProblemC()
+        c.params = capi.ModelParamsC(1.3, 0.5, 0.2, 1.0, 0.01, 1.0, 1.0)
+        c.integrator, c.signs_on = ig, 1
+        c.qoi.kind, c.qoi.r, c.qoi.a, c.qoi.b, c.qoi.delta = 0, 4, 0.1055, 0.1555, 0.1
+        c.x0, c.u0, c.T, c.m0, c.seed = 0.5, 0.1, 1.0, 1, SEED
+        c.adaptive, c.x_adapt, c.profile = 0, 0.05, 0
+        self._c = c
+
+
+def workload_config(a, world: int) -> dict:
+    """`config` of BOTH arms (identical, so the driver can compare them): the
+    C5 workload.  The CPU arm times a bounded sample of it (reported outside
+    `config`); throughput per path-step does not depend on the path count."""
+    Mf = 1 << a.level
+    return {"workload": f"C5: level {a.level} coupled pair ({Mf} fine + {Mf // 2} coarse steps), "
+                        f"{a.integrator}, reference profile, x0=0.5, u0=0.1, T=1, M0=1, "
+                        f"mean-position QoI, Philox seed {SEED}",
+            "paths_per_gpu": a.paths, "level": a.level, "integrator": a.integrator,
+            "l2": "GPU arm: flushed between timed steps (256 MB write); path state is "
+                  "register-resident",
+            "parallelism": f"dp{world} (contiguous super-block shards, one native NCCL "
+                           f"all-gather of the partials per step)"}
+
+
 def host_threads() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -70,7 +104,7 @@ def host_threads() -> int:
 
 
 # ------------------------------------------------------------ CPU reference
-def reference_sample(ig: int, level: int, target_s: float, threads: int):
+def reference_sample(ig: int, level: int, target_s: float, threads: int, pr=None):
     """Time the reference's own accumulate_samples (oracle/_ref, unmodified
     headers, std::thread pool) on a bounded sample; returns (path-steps/s,
     samples, seconds)."""
@@ -79,7 +113,7 @@ def reference_sample(ig: int, level: int, target_s: float, threads: int):
     R = O.ref()
     if R is None:
         raise RuntimeError("oracle/_ref/libablmc_ref.so is missing (built by __graft_entry__.build)")
-    pr = problem_c(ig)
+    pr = pr or problem_c(ig)
     Mf = 1 << level
     n = max(threads * 64, 4096)
     secs = C.c_double()
@@ -96,17 +130,21 @@ def reference_sample(ig: int, level: int, target_s: float, threads: int):
 
 
 def run_reference(a):
+    """The reference arm: the unmodified reference's own accumulate_samples
+    (oracle/_ref, std::thread pool on every host thread) on the C5 workload,
+    each step a bounded sample of it.  Under torchrun only rank 0 runs.  The
+    product library is never loaded here."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return  # rank 0 alone runs the CPU reference arm
     ig = {"se": 0, "gl": 1, "baoab": 2}[a.integrator]
     threads = host_threads()
-    step_s = max(1.0, 60.0 / max(1, a.steps + a.warmup))  # whole run within ~1-2 min
-    rate, n, _ = reference_sample(ig, a.level, step_s, threads)
+    pr = _RefProblem(ig)
+    step_s = a.ref_step_seconds or max(1.0, 60.0 / max(1, a.steps + a.warmup))  # run ~1-2 min
+    rate, n, _ = reference_sample(ig, a.level, step_s, threads, pr)
     sys.path.insert(0, str(ROOT / "tests"))
     import oracle_lib as O
     R = O.ref()
-    pr = problem_c(ig)
     secs = C.c_double()
     times = []
     for i in range(a.warmup + a.steps):
@@ -118,18 +156,18 @@ def run_reference(a):
     Mf = 1 << a.level
     t = statistics.mean(times)
     value = n * Mf / t
+    sample = (f"{n} coupled paths x {Mf} fine steps per step (bounded sample of the workload); "
+              f"reference accumulate_samples with {threads} worker threads")
     line = {
         "impl": "reference", "metric": "coupled fine path-steps/s (level sampler)",
         "value": value, "unit": "path-steps/s", "n_gpus": a.gpus, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (Philox seed 42)",
-        "config": {"workload": f"C5: level {a.level} coupled pair, {IG_NAME[ig]}, reference profile, "
-                               f"x0=0.5, u0=0.1, T=1, M0=1; bounded CPU sample of {n} paths/step",
-                   "level": a.level, "paths_per_step": n},
+        "config": workload_config(a, a.gpus),
+        "cpu_sample": {"paths_per_step": n, "note": "throughput per path-step does not depend on "
+                       "the number of paths (independent samples)"},
         "cpu_baseline": {"value": value, "unit": "path-steps/s", "cores": threads,
-                         "kind": "reference",
-                         "sample": f"{n} coupled paths x {Mf} fine steps per step; reference "
-                                   f"accumulate_samples with {threads} worker threads"},
+                         "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": "path-steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -395,7 +433,6 @@ def mlmc_sweep(a):
 
 # ---------------------------------------------------------------- B200 arm
 def run_b200(a):
-    import numpy as np
     import torch
     import torch.distributed as dist
     from paper_1612_07717_b200 import ablmc
@@ -408,20 +445,26 @@ def run_b200(a):
     torch.cuda.set_device(local)
     dist_on = world > 1 or a.force_dist
     if dist_on:
-        # NCCL's own log lines ("NCCL version ..." with this image's
-        # NCCL_DEBUG=VERSION) go to stderr: stdout carries only the JSON line.
-        # device_id makes the communicator initialisation eager, inside here.
+        # torch.distributed is the plumbing here (barriers, max over ranks,
+        # shipping the NCCL unique id); the data path is the library's own NCCL
+        # communicator.  NCCL's own log lines ("NCCL version ..." with this
+        # image's NCCL_DEBUG=VERSION) go to stderr: stdout carries only the
+        # JSON line.
         sys.stdout.flush()
         saved = os.dup(1)
         os.dup2(2, 1)
         try:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
             dist.barrier()
+            ablmc.init(local)
+            from paper_1612_07717_b200.sharding import init_nccl_group
+            init_nccl_group()  # native group: ablmc_init_group(local, rank, world, id)
         finally:
             sys.stdout.flush()
             os.dup2(saved, 1)
             os.close(saved)
-    ablmc.init(local)
+    else:
+        ablmc.init(local)
     # A dedicated (non-default) stream shared by torch and the library, so the
     # CUDA events below bracket exactly the library's kernels.
     stream = torch.cuda.Stream()
@@ -434,7 +477,6 @@ def run_b200(a):
     Mf = 1 << level
     N = a.paths
     pr = problem_c(ig)
-    first = rank * N
     pc = C.byref(pr._c)
 
     def barrier():
@@ -450,21 +492,16 @@ def run_b200(a):
         return float(t.item())
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
-    res_s = torch.zeros(2, dtype=torch.float64, device="cuda")
-    res_c = torch.zeros(3, dtype=torch.int64, device="cuda")  # n, failed, cost_steps
-    gat_s = torch.zeros(world, 2, dtype=torch.float64, device="cuda")
-    gat_c = torch.zeros(world, 3, dtype=torch.int64, device="cuda")
 
     def device_step():
-        rc = lib.ablmc_accumulate_device(pc, level, first, N)
+        # the whole job's index range [0, world N): in the native group each
+        # rank samples its contiguous super-blocks ([r N, (r+1) N) when N is a
+        # multiple of 2^22), then ONE all-gather of the partials and the
+        # ordered device merge -- every rank ends with the job's moments
+        rc = lib.ablmc_accumulate_device(pc, level, 0, world * N)
         if rc:
             ablmc._check(rc)
-        launches = lib.ablmc_last_launch_count()
-        if dist_on:  # one collective per step: all-gather of the per-rank moments
-            lib.ablmc_copy_device_result(C.c_void_p(res_s.data_ptr()), C.c_void_p(res_c.data_ptr()))
-            dist.all_gather_into_tensor(gat_s, res_s)
-            dist.all_gather_into_tensor(gat_c, res_c)
-        return launches
+        return lib.ablmc_last_launch_count(), lib.ablmc_last_collective_count()
 
     # ---- value: device-resident, CUDA events on the launching stream
     for _ in range(a.warmup):
@@ -472,7 +509,7 @@ def run_b200(a):
     barrier()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(a.steps)]
-    launches = 0
+    launches = collectives = 0
     k1_ms, k1_n = C.c_double(), C.c_int64()
     lib.ablmc_level_kernel_times(C.byref(k1_ms), C.byref(k1_n))  # reset
     lib.ablmc_set_profiling(1)
@@ -481,8 +518,10 @@ def run_b200(a):
             flush.zero_()  # L2 flush between timed iterations (outside the events)
             barrier()
             ev[i][0].record(stream)
-            launches += device_step()
+            nl, nc = device_step()
             ev[i][1].record(stream)
+            launches += nl
+            collectives += nc
         barrier()
     lib.ablmc_set_profiling(0)
     lib.ablmc_level_kernel_times(C.byref(k1_ms), C.byref(k1_n))
@@ -494,22 +533,19 @@ def run_b200(a):
     ms_per_step = total_ms / a.steps
     value = world * N * Mf / (ms_per_step * 1e-3)
 
-    # moments of the last step (sanity: E[Y_10], all ranks)
+    # moments of the last step (sanity: E[Y_10] of the whole job, every rank)
     acc = ablmc.LevelStats().init(level, pr.h_level(level), 1)
     v = acc._view()
     ablmc._check(lib.ablmc_fetch_device_result(pc, level, C.byref(v)))
     acc._take(v)
 
-    # ---- dominant kernel share: level kernel alone, one launch, events
-    # (N paths in one chunk of 2^25 -> one K1 launch dominates the step)
     fp64_rate = C.c_double()
     ablmc._check(lib.ablmc_probe_fp64_rate(C.byref(fp64_rate)))
-    # dominant kernel (K1, the fused level sampler): algorithmic FP64-pipe ops
-    # per launch / its average launch duration (CUDA events on its stream)
-    achieved = steps_per_launch * W_ALG[ig] / (k1_avg_ms * 1e-3)
     peak = fp64_rate.value
-    # DRAM bytes per K1 launch and executed FP64-pipe instructions, scaled from
-    # the committed ncu capture of the same kernel (profiles/k1_ncu.json)
+    # dominant kernel (K1, the fused level sampler): FP64-pipe instructions
+    # per coupled fine path-step as executed (ncu, profiles/k1_ncu.json: the
+    # floor of the bit-exact algorithm as implemented) x path-steps per launch
+    # / its average launch duration (CUDA events on its stream)
     traffic, w_exec = None, None
     tp = ROOT / "profiles" / "k1_ncu.json"
     if tp.exists():
@@ -517,16 +553,16 @@ def run_b200(a):
         if "dram_bytes_per_path_step" in prof:
             traffic = prof["dram_bytes_per_path_step"] * steps_per_launch
             w_exec = prof["fp64_instr_per_path_step"]
+    kernel_rate = steps_per_launch / (k1_avg_ms * 1e-3)  # path-steps/s inside K1
+    w = w_exec if w_exec is not None else W_ALG[ig]
+    achieved = kernel_rate * w
 
     # ---- e2e: the public API call a user makes (accumulate_samples into a
-    # host LevelStats) over the whole job's index range [0, world N); with
-    # several ranks the library's collective splits it by super-blocks
-    # (rank r gets [r N, (r+1) N)) and all-gathers the partials once per call.
-    if dist_on:
-        from paper_1612_07717_b200.sharding import disable_collective, enable_collective
-        enable_collective()
+    # host LevelStats) over the whole job's index range [0, world N): with the
+    # native group the library splits it by super-blocks and all-gathers the
+    # partials once per call; host<->device traffic inside the timed region
     e2e_times = []
-    n_sb = ablmc.num_superblocks(N)
+    n_sb = ablmc.num_superblocks(world * N)
     for i in range(a.warmup + a.steps):
         barrier()
         t0 = time.perf_counter()
@@ -535,16 +571,18 @@ def run_b200(a):
         t1 = time.perf_counter()
         if i >= a.warmup:
             e2e_times.append(t1 - t0)
-    if dist_on:
-        disable_collective()
     e2e_t = max_over_ranks(statistics.mean(e2e_times))
     e2e_value = world * N * Mf / e2e_t
     h2d = C.sizeof(pr._c)  # the problem descriptor (kernel parameters) per call
-    d2h = n_sb * (2 * 1 + 2) * 8  # this rank's super-block partials
+    # the gathered block (all ranks' partial rows + status rows) or, on one
+    # device, this rank's super-block partials
+    rows = (n_sb + world - 1) // world
+    d2h = (world * (rows + 1) * (2 + 3) * 8) if dist_on else n_sb * (2 + 3) * 8
 
     if rank != 0:
         if dist_on:
             dist.barrier()
+            ablmc.init(local)
             dist.destroy_process_group()
         return
 
@@ -553,29 +591,27 @@ def run_b200(a):
         "unit": "path-steps/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (Philox seed 42)",
-        "config": {"workload": f"C5: level {level} coupled pair ({Mf} fine + {Mf // 2} coarse steps), "
-                               f"{IG_NAME[ig]}, reference profile, x0=0.5, u0=0.1, T=1, M0=1, "
-                               f"mean-position QoI",
-                   "paths_per_gpu": N, "level": level, "integrator": IG_NAME[ig],
-                   "l2": "flushed between timed steps (256 MB write); kernel state is register-resident",
-                   "parallelism": f"dp{world} (sample shards, 1 NCCL all-gather/step)"},
+        "config": workload_config(a, world),
         "e2e": {"value": e2e_value, "unit": "path-steps/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
+        "collectives": {"per_step": collectives / a.steps,
+                        "kind": "ncclAllGather on the library's own communicator" if dist_on
+                                else "none (one device)"},
         "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12,
                      "unit": "FP64 Tops/s (pipe lane-ops)", "frac": achieved / peak,
                      "traffic": traffic,
                      "kernel": "k_level (K1, fused coupled level sampler)",
                      "kernel_avg_ms": k1_avg_ms, "kernel_share_of_step": k1_share,
                      "path_steps_per_launch": steps_per_launch,
-                     "W_alg": W_ALG[ig], "W_executed_ncu": w_exec,
-                     "frac_executed": (None if w_exec is None else
-                                       steps_per_launch * w_exec / (k1_avg_ms * 1e-3) / peak),
-                     "note": f"achieved = coupled fine path-steps per K1 launch x W_alg="
-                             f"{W_ALG[ig]:.0f} FP64-pipe ops per path-step (SURVEY.md 8(d)'s "
-                             "algorithmic count) / K1 launch time; frac_executed uses the FP64-pipe "
-                             "instructions ncu counts for this kernel (profiles/k1_ncu.json), i.e. "
-                             "the pipe utilisation; peak = DFMA probe measured in this run "
+                     "W_executed_ncu": w_exec, "W_alg_survey": W_ALG[ig],
+                     "frac_W_alg_survey": kernel_rate * W_ALG[ig] / peak,
+                     "note": f"achieved = coupled fine path-steps per K1 launch x W = {w:.1f} "
+                             "FP64-pipe instructions per path-step as executed (ncu, "
+                             "profiles/k1_ncu.json: DFMA/DMUL/DADD/DSETP/MUFU64 of the bit-exact "
+                             "algorithm) / K1 launch time, i.e. the FP64-pipe utilisation; "
+                             "frac_W_alg_survey uses SURVEY.md 8(d)'s libdevice-based count "
+                             f"{W_ALG[ig]:.0f} instead; peak = DFMA probe measured in this run "
                              "(MEASURED_PEAKS.json has no FP64 entry); traffic = ncu DRAM bytes "
                              "per path-step x path-steps per launch"},
         "clocks": clk.summary(),
@@ -597,11 +633,33 @@ def run_b200(a):
     print(json.dumps(line), flush=True)
     if dist_on:
         dist.barrier()
+        ablmc.init(local)
         dist.destroy_process_group()
+
+
+def free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def maybe_spawn(a) -> None:
+    """`bench.py --gpus N` outside torchrun: re-exec under
+    torch.distributed.run with one rank per GPU (the driver may also launch
+    it under torchrun itself; then WORLD_SIZE is set and nothing happens)."""
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={a.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+               str(free_port()), str(Path(__file__).resolve()), *sys.argv[1:]]
+        os.execv(sys.executable, cmd)
 
 
 def main():
     a = parse()
+    maybe_spawn(a)
     if a.impl == "reference":
         run_reference(a)
     else:

@@ -80,6 +80,16 @@ inline ablmc_level_stats view(ablmc::LevelStats& st) {
   return v;
 }
 
+// The reference fans accumulate_samples out over `workers` threads in one
+// process (stats.hpp:120-135); the device analogue is one process driving n
+// GPUs: after init_devices(n) every accumulate call below -- and so every
+// iteration of a driver loop built on it -- shards its super-blocks over the
+// n GPUs and exchanges the partials in ONE NCCL all-gather, with the same
+// bits as one GPU.  Without it the library uses one device.
+inline void init_devices(int n, const int* devices = nullptr) {
+  check(ablmc_init_devices(n, devices));
+}
+
 // accumulate_samples(acc, first, count, workers, pr.level_sampler(level))
 inline void accumulate_samples(ablmc::LevelStats& acc, std::int64_t first, std::int64_t count,
                                const ablmc::Problem& pr, int level) {

@@ -11,6 +11,16 @@
 
 int main(int argc, char** argv) {
   const int n = argc > 1 ? std::atoi(argv[1]) : 20000;
+  // optional: shard over this many GPUs of this process (ablmc_init_devices)
+  const int gpus = argc > 2 ? std::atoi(argv[2]) : 0;
+  if (gpus > 0) {
+    try {
+      ablmc_b200::init_devices(gpus);
+    } catch (const std::exception& e) {
+      std::printf("device error: %s\n", e.what());
+      return 3;
+    }
+  }
   const ablmc::Problem pr = ablmc::Problem::make(ablmc::ModelParams{}, ablmc::Integrator::gl,
                                                  ablmc::QoISpec{}, 0.05, 0.1, 1.0, 40, 77);
   for (int l = 0; l <= 3; ++l) {

@@ -75,6 +75,44 @@ def init(device: int = -1) -> None:
     _check(lib().ablmc_init(device))
 
 
+def init_devices(n: int, devices: Sequence[int] | None = None) -> None:
+    """Drive n GPUs from this process (the reference's single-process
+    fan-out, stats.hpp:120-135): every accumulate call, and so every driver
+    iteration, shards its super-blocks over them and exchanges the partials
+    in ONE NCCL all-gather (include/ablmc_b200.h, multi-GPU sharding)."""
+    devs = None if devices is None else (C.c_int * n)(*[int(d) for d in devices])
+    _check(lib().ablmc_init_devices(int(n), devs))
+
+
+def nccl_unique_id() -> bytes:
+    """ncclUniqueId for ablmc_init_group (rank 0 creates it and ships it)."""
+    buf = (C.c_ubyte * capi.ABLMC_NCCL_ID_BYTES)()
+    _check(lib().ablmc_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def init_group(device: int, rank: int, world: int, unique_id: bytes) -> None:
+    """One process per GPU: join the library's own NCCL communicator."""
+    if len(unique_id) != capi.ABLMC_NCCL_ID_BYTES:
+        raise ValueError("unique_id must be ABLMC_NCCL_ID_BYTES long")
+    buf = (C.c_ubyte * capi.ABLMC_NCCL_ID_BYTES).from_buffer_copy(unique_id)
+    _check(lib().ablmc_init_group(int(device), int(rank), int(world), buf))
+
+
+def group_info() -> dict:
+    m, r, w, n = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    lib().ablmc_group_info(C.byref(m), C.byref(r), C.byref(w), C.byref(n))
+    return {"mode": m.value, "rank": r.value, "world": w.value, "n_local": n.value}
+
+
+def last_collective_count() -> int:
+    return int(lib().ablmc_last_collective_count())
+
+
+def finalize() -> None:
+    _check(lib().ablmc_finalize())
+
+
 def set_stream(cuda_stream: int | None) -> None:
     """Launch on this cudaStream_t (e.g. ``torch.cuda.Stream().cuda_stream``).
     0/None selects the library's own stream (NOT the legacy default stream)."""
@@ -330,6 +368,35 @@ def merge_partials(acc: LevelStats, pr: Problem, level: int, sums: np.ndarray, c
                                       sums.ctypes.data_as(C.POINTER(C.c_double)),
                                       counts.ctypes.data_as(C.POINTER(C.c_int64)), _P(v)))
     acc._take(v)
+
+
+def gather_layout(dim: int, world: int, n_sb: Sequence[int]) -> tuple[int, int, list[int]]:
+    """(rows per rank, row width in doubles, first row of each request) of
+    the all-gather block of a batch of requests of n_sb[q] super-blocks
+    (include/ablmc_b200.h)."""
+    n = len(n_sb)
+    cs = (C.c_int64 * max(n, 1))(*[int(c) for c in n_sb])
+    rows, width = C.c_int64(), C.c_int64()
+    base = (C.c_int64 * max(n, 1))()
+    _check(lib().ablmc_gather_layout(int(dim), int(world), n, cs, C.byref(rows), C.byref(width),
+                                     base))
+    return rows.value, width.value, list(base)[:n]
+
+
+def merge_gathered(accs: Sequence[LevelStats], n_sb: Sequence[int], world: int,
+                   recv: np.ndarray) -> None:
+    """Merge all ranks' gathered blocks (recv, rank-major) into accs in
+    global super-block order -- the library's post-all-gather step."""
+    n = len(accs)
+    dim = accs[0].dim
+    recv = np.ascontiguousarray(recv, dtype=np.float64)
+    views = [a._view() for a in accs]
+    cs = (C.c_int64 * n)(*[int(c) for c in n_sb])
+    ptrs = (C.POINTER(capi.LevelStatsC) * n)(*[_P(v) for v in views])
+    _check(lib().ablmc_merge_gathered(int(dim), int(world), n, cs,
+                                      recv.ctypes.data_as(C.POINTER(C.c_double)), ptrs))
+    for a, v in zip(accs, views):
+        a._take(v)
 
 
 # ------------------------------------------------------------- oracle mode

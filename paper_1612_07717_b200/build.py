@@ -16,7 +16,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OBJ = PKG / "build"
 LIB = PKG / "libablmc_b200.so"
-SOURCES = ["level_kernels.cu", "adaptive_kernels.cu", "binned_kernels.cu", "capi.cu", "drivers.cu",
+SOURCES = ["level_kernels.cu", "adaptive_kernels.cu", "binned_kernels.cu", "collective.cu", "capi.cu", "drivers.cu",
            "output.cpp"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -21,6 +21,7 @@ ABLMC_ERR_NO_DEVICE = 5
 ABLMC_SUPERBLOCK = 1 << 22
 ABLMC_NCOUNTS = 3  # {n, failed, cost_steps} per super-block partial
 ABLMC_MAX_LEVELS = 24
+ABLMC_NCCL_ID_BYTES = 128
 
 SE, GL, BAOAB = 0, 1, 2
 QOI_MEAN_POSITION, QOI_SMOOTHED_INDICATOR, QOI_RAW_INDICATOR, QOI_BINNED_FIELD = 0, 1, 2, 3
@@ -114,6 +115,15 @@ ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, P(C.c_double), C.c_int64, P(C.c_
 # name -> (restype, argtypes): every symbol include/ablmc_b200.h declares.
 SIGNATURES = {
     "ablmc_set_collective": (C.c_int, [C.c_int, C.c_int, ALLGATHER_FN, C.c_void_p]),
+    "ablmc_nccl_unique_id": (C.c_int, [P(C.c_ubyte)]),
+    "ablmc_init_group": (C.c_int, [C.c_int, C.c_int, C.c_int, P(C.c_ubyte)]),
+    "ablmc_init_devices": (C.c_int, [C.c_int, P(C.c_int)]),
+    "ablmc_group_info": (C.c_int, [P(C.c_int), P(C.c_int), P(C.c_int), P(C.c_int)]),
+    "ablmc_last_collective_count": (C.c_int64, []),
+    "ablmc_gather_layout": (C.c_int, [C.c_int, C.c_int, C.c_int, P(C.c_int64), P(C.c_int64),
+                                      P(C.c_int64), P(C.c_int64)]),
+    "ablmc_merge_gathered": (C.c_int, [C.c_int, C.c_int, C.c_int, P(C.c_int64), P(C.c_double),
+                                       P(P(LevelStatsC))]),
     "ablmc_abi_version": (C.c_int, []),
     "ablmc_init": (C.c_int, [C.c_int]),
     "ablmc_finalize": (C.c_int, []),

@@ -121,6 +121,14 @@ cudaError_t launch_binned(const KernelArgs& a, bool coupled, double* tile_sums,
                           const long long* tile_cnt, cudaStream_t st);
 cudaError_t launch_merge_super(int64_t n_sb, int dim, const double* ss, const long long* sc,
                                double* rs, long long* rc, cudaStream_t st);
+// collective.cu: pack rows [0, rows) of the super-block partials plus one
+// status row into the all-gather send buffer; merge one request's gathered
+// rows (all ranks) in global super-block order into the device result.
+cudaError_t launch_pack_rows(int64_t rows, int dim, const double* sb_sums, const long long* sb_cnt,
+                             double* send, long long status, cudaStream_t st);
+cudaError_t launch_merge_gathered(int world, int64_t cap_total, int64_t n_sb, int64_t pbase,
+                                  int dim, const double* recv, double* res_sums,
+                                  long long* res_cnt, long long* res_status, cudaStream_t st);
 cudaError_t upload_log_table();           // Box-Muller log table (ablmc_init), one
 cudaError_t upload_log_table_adaptive();  // per translation unit that draws normals
 cudaError_t launch_normals(uint32_t k0, uint32_t k1, uint64_t idx, uint64_t kstart, int64_t n,

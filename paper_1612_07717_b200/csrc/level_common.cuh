@@ -16,7 +16,7 @@ namespace {
 using namespace ablmc_dev;
 
 #ifndef ABLMC_PEEL_WINDOWS
-#define ABLMC_PEEL_WINDOWS 16  // hoisted window 0 up to level 5 (GL/BAOAB, reference profile)
+#define ABLMC_PEEL_WINDOWS 16  // hoisted window 0 for M <= 32 fine steps (GL/BAOAB, reference profile)
 #endif
 constexpr int kTile = ABLMC_TILE;            // samples per CTA (one per thread)
 constexpr int kWarps = kTile / 32;
@@ -193,8 +193,10 @@ __device__ __forceinline__ PathOut run_sample(const KernelArgs& a, uint64_t idx,
   };
   const int64_t windows = a.M >> 1;
   // Window 0 with both legs' first steps from the host (first_step_finish).
-  // Used for level 1 (one window) and, reference profile GL/BAOAB, levels 2-5
-  // (the coupled levels with the most samples).  Higher levels keep the
+  // Used for paths of M = 2 fine steps (one window) and, reference profile
+  // GL/BAOAB, of M <= 2 ABLMC_PEEL_WINDOWS = 32 (levels 1 and 2-5 when m0 =
+  // 1, as in the bench's configs; with the reference's default m0 = 40 every
+  // coupled level has M >= 80 and runs the loop).  Longer paths keep the
   // single-body loop: there the hoisting is worth < 2%, and a window peeled
   // in front of the SE loop -- or of the extension profiles' loops -- costs
   // them spills.
@@ -237,19 +239,19 @@ __device__ __forceinline__ PathOut run_sample(const KernelArgs& a, uint64_t idx,
     return ok;
   };
   constexpr bool kPeelMore = IG != kSE && PROF == kProfileReference;
-  if (a.fs_ok && windows == 1) {  // level 1: the whole sample
+  if (a.fs_ok && windows == 1) {  // M = 2: the whole sample
     o.ok = window0_hoisted();
     return o;
   }
-  if (kPeelMore && a.fs_ok && windows <= ABLMC_PEEL_WINDOWS) {  // levels 2-5
+  if (kPeelMore && a.fs_ok && windows <= ABLMC_PEEL_WINDOWS) {  // 4 <= M <= 32
     bool ok = window0_hoisted();
     for (int64_t n = 1; ok && !(FAST && bad) && n < windows; ++n) ok = window(std::false_type{}, n);
     o.ok = ok;
     return o;
   }
   if (IG != kBAOAB && windows == 1) {
-    // level 1 (M = 2, the coupled level with the most samples): one window,
-    // both legs at x0.  (Peeling window 0 in front of the loop for every
+    // M = 2 (level 1 when m0 = 1, the coupled level with the most samples):
+    // one window, both legs at x0.  (Peeling window 0 in front of the loop for every
     // level instead costs the SE loop ~200 B of spills.)
     o.ok = window(std::true_type{}, 0);
     return o;

@@ -1,17 +1,29 @@
-"""Multi-GPU sharding of one accumulate call.
+"""Multi-GPU sharding of accumulate calls.
 
-One process per GPU.  The sample indices [first, first+count) are cut into
-super-blocks of ``ABLMC_SUPERBLOCK`` samples; rank r computes a contiguous
-range of super-blocks on its GPU (``ablmc_accumulate_partials``), ONE
-collective (all-gather over ``torch.distributed``: NCCL on GPUs, gloo in the
-CPU tests) moves the per-super-block partials, and every rank merges all of
-them in index order (``ablmc_merge_partials``).  The merged bits are identical
-for any world size, like the reference's worker-count invariance
-(stats.hpp:93-95, test_estimators.cpp:97-108).
+The library shards natively (include/ablmc_b200.h, "multi-GPU sharding"):
+sample indices are cut into super-blocks of ``ABLMC_SUPERBLOCK`` samples,
+each rank computes a contiguous, balanced range of them, ONE all-gather per
+accumulate call -- per ``accumulate_levels`` batch, i.e. per MLMC allocation
+round -- moves the per-super-block partials, and every rank merges all of
+them in index order.  The merged bits are identical for any world size, like
+the reference's worker-count invariance (stats.hpp:120-135,
+test_estimators.cpp:97-108).
+
+This module only forms the group from Python:
+
+* ``init_nccl_group`` -- one process per GPU (torchrun): rank 0's
+  ``ncclUniqueId`` travels over the torch.distributed group, then the library
+  joins its OWN NCCL communicator; the data path is device to device inside
+  the library (no Python, no host staging);
+* ``enable_collective`` -- a host all-gather callback over a torch.distributed
+  group (gloo on CPU hosts, or ranks sharing a GPU);
+* ``accumulate_sharded_levels`` -- the same exchange written out in Python
+  around ``accumulate_partials`` (or any partials function: the CPU tests feed
+  oracle partials), finishing with the library's own ``merge_gathered``.
 """
 from __future__ import annotations
 
-from typing import Callable, Optional
+from typing import Callable, Optional, Sequence
 
 import numpy as np
 
@@ -19,14 +31,30 @@ from . import ablmc, capi
 
 
 _collective_keepalive = None
+collective_calls = 0  # host all-gathers issued through enable_collective's callback
+
+
+def init_nccl_group(group=None, device: Optional[int] = None) -> None:
+    """Join the library's native NCCL group: this process's GPU becomes rank
+    ``dist.get_rank(group)`` of ``dist.get_world_size(group)``."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = torch.cuda.current_device() if device is None else int(device)
+    obj = [ablmc.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group else 0,
+                               group=group)
+    ablmc.init_group(dev, rank, world, obj[0])
 
 
 def enable_collective(group=None) -> None:
     """Route every accumulate call of the library (and so every iteration of
-    run_mlmc / run_stmc / decay_sweep) through this process group: each rank
-    computes its contiguous super-block range and ONE all-gather per call
-    (NCCL over NVLink for an "nccl" group; gloo on host for a CPU group)
-    exchanges the partials (ablmc_set_collective in include/ablmc_b200.h)."""
+    run_mlmc / run_stmc / decay_sweep) through this process group with a host
+    all-gather callback (ablmc_set_collective): each rank computes its
+    super-block range and ONE all-gather per call/batch exchanges the block
+    of packed partials."""
     import torch
     import torch.distributed as dist
 
@@ -37,12 +65,14 @@ def enable_collective(group=None) -> None:
     dev = torch.device("cuda", torch.cuda.current_device()) if nccl else torch.device("cpu")
 
     def allgather(ctx, send, count, recv):
+        global collective_calls
+        collective_calls += 1
         try:
             src = np.ctypeslib.as_array(send, (count,))
             t = torch.from_numpy(src.copy()).to(dev)
-            outs = [torch.empty_like(t) for _ in range(world)]
-            dist.all_gather(outs, t, group=group)
-            np.ctypeslib.as_array(recv, (world * count,))[:] = torch.cat(outs).cpu().numpy()
+            out = torch.empty(world * count, dtype=t.dtype, device=dev)
+            dist.all_gather_into_tensor(out, t, group=group)
+            np.ctypeslib.as_array(recv, (world * count,))[:] = out.cpu().numpy()
             return 0
         except Exception:  # noqa: BLE001 - reported to the C side as a failed collective
             return 1
@@ -68,43 +98,49 @@ def shard_superblocks(n_sb: int, rank: int, world: int) -> tuple[int, int]:
 PartialsFn = Callable[[ablmc.Problem, int, int, int, int, int], tuple]
 
 
+def accumulate_sharded_levels(requests: Sequence[tuple], pr: ablmc.Problem, group=None,
+                              partials_fn: Optional[PartialsFn] = None,
+                              superblock: int = capi.ABLMC_SUPERBLOCK,
+                              fail_status: int = 0) -> None:
+    """accumulate_levels over all ranks of `group` with ONE all-gather:
+    requests are (acc, first, count, level); every rank ends with the same
+    accs.  The block layout and the merge are the library's
+    (gather_layout / merge_gathered); fail_status != 0 makes this rank
+    report a failed share (every rank then raises)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    fn = partials_fn or (lambda p, l, f, c, a, b: ablmc.accumulate_partials(p, l, f, c, a, b))
+    dim = pr.dim()
+    n_sb = [max(0, (int(c) + superblock - 1) // superblock) for _, _, c, _ in requests]
+    rows, width, base = ablmc.gather_layout(dim, world, n_sb)
+    block = np.zeros(((rows + 1), width))
+    status = fail_status
+    if status == 0:
+        try:
+            for q, (acc, first, count, level) in enumerate(requests):
+                lo, hi = shard_superblocks(n_sb[q], rank, world)
+                if hi > lo:
+                    sums, cnts = fn(pr, level, first, count, lo, hi)
+                    block[base[q]: base[q] + hi - lo, : 2 * dim] = sums
+                    block[base[q]: base[q] + hi - lo, 2 * dim:] = np.asarray(cnts, np.int64).view(
+                        np.float64)
+        except ablmc.CudaError:
+            status = capi.ABLMC_ERR_CUDA
+    block[rows, 0] = np.array([status], np.int64).view(np.float64)[0]
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    t = torch.from_numpy(block.reshape(-1)).to(dev)
+    out = torch.empty(world * t.numel(), dtype=t.dtype, device=dev)
+    dist.all_gather_into_tensor(out, t, group=group)  # the one collective
+    ablmc.merge_gathered([r[0] for r in requests], n_sb, world, out.cpu().numpy())
+
+
 def accumulate_sharded(acc: ablmc.LevelStats, first: int, count: int, pr: ablmc.Problem,
                        level: int, group=None, partials_fn: Optional[PartialsFn] = None,
                        superblock: int = capi.ABLMC_SUPERBLOCK) -> None:
     """accumulate_samples(acc, first, count, ., pr.level_sampler(level)) over
     all ranks of `group`; every rank ends with the same `acc`."""
-    import torch
-    import torch.distributed as dist
-
-    if count <= 0:
-        return
-    world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
-    n_sb = (count + superblock - 1) // superblock
-    lo, hi = shard_superblocks(n_sb, rank, world)
-    fn = partials_fn or (lambda p, l, f, c, a, b: ablmc.accumulate_partials(p, l, f, c, a, b))
-    dim = pr.dim()
-    if hi > lo:
-        sums, cnts = fn(pr, level, first, count, lo, hi)
-    else:
-        sums, cnts = np.zeros((0, 2 * dim)), np.zeros((0, capi.ABLMC_NCOUNTS), dtype=np.int64)
-    # pack (sums | counts as exact float64 bit patterns) into one buffer per rank
-    width = 2 * dim + capi.ABLMC_NCOUNTS
-    cap = (n_sb + world - 1) // world
-    buf = np.zeros((cap, width))
-    buf[: hi - lo, : 2 * dim] = sums
-    buf[: hi - lo, 2 * dim:] = cnts.view(np.float64)
-    backend = dist.get_backend(group)
-    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
-    t = torch.from_numpy(buf).to(dev)
-    outs = [torch.empty_like(t) for _ in range(world)]
-    dist.all_gather(outs, t, group=group)  # the one collective
-    allb = torch.stack(outs).cpu().numpy()
-    rows = []
-    for r in range(world):
-        a, b = shard_superblocks(n_sb, r, world)
-        rows.append(allb[r, : b - a])
-    merged = np.concatenate(rows, axis=0)
-    s = np.ascontiguousarray(merged[:, : 2 * dim])
-    c = np.ascontiguousarray(merged[:, 2 * dim:]).view(np.int64)
-    ablmc.merge_partials(acc, pr, level, s, c)
+    accumulate_sharded_levels([(acc, first, count, level)], pr, group, partials_fn, superblock)

@@ -46,8 +46,14 @@ def main():
     single = run()
     enable_collective()
     shared = run()
+    # one allocation round of four levels: ONE all-gather
+    from paper_1612_07717_b200 import sharding
+    c0 = sharding.collective_calls
+    reqs = [(ablmc.LevelStats().init(l, pr.h_level(l), 1), 0, 1000 << (4 - l), l) for l in range(4)]
+    ablmc.accumulate_levels(reqs, pr)
+    one_per_round = sharding.collective_calls - c0 == 1 and ablmc.last_collective_count() == 1
     disable_collective()
-    ok = single == shared
+    ok = single == shared and one_per_round
     print(f"rank {dist.get_rank()}/{world} ({backend}) collective == single-process: {ok}",
           flush=True)
     dist.barrier()

@@ -1,0 +1,98 @@
+"""The library's native multi-GPU path in ONE process (ablmc_init_devices:
+one context and stream per GPU, an NCCL clique, one device-to-device
+all-gather per accumulate call / per accumulate_levels batch): bit-identical
+to the single-device calls.  On a one-GPU box the clique has one member, so
+this exercises the packing, the NCCL all-gather, the status row and both
+merges (host and device-resident) at world size 1; tests/test_sharding.py
+covers the layout and merge for world sizes 2-3 on CPU."""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from paper_1612_07717_b200 import ablmc
+
+pytestmark = pytest.mark.gpu
+
+
+def _device_result(pr, level, first, count):
+    lib = ablmc.lib()
+    ablmc._check(lib.ablmc_accumulate_device(C.byref(pr._c), level, first, count))
+    d = ablmc.LevelStats().init(level, pr.h_level(level), pr.dim())
+    v = d._view()
+    ablmc._check(lib.ablmc_fetch_device_result(C.byref(pr._c), level, C.byref(v)))
+    d._take(v)
+    return d
+
+
+def _key(s):
+    return (s.sum_y.tobytes(), s.sum_y2.tobytes(), s.n, s.failed, s.cost_steps)
+
+
+def _workload(pr, prb, count):
+    out = {}
+    a = ablmc.LevelStats().init(2, pr.h_level(2), 1)
+    ablmc.accumulate_samples(a, 5, count, pr, 2)
+    out["samples"] = _key(a)
+    out["samples_collectives"] = ablmc.last_collective_count()
+    reqs = [(ablmc.LevelStats().init(l, pr.h_level(l), 1), 7 * l, (count >> l) + l, l)
+            for l in range(5)]
+    ablmc.accumulate_levels(reqs, pr)
+    out["levels"] = [_key(r[0]) for r in reqs]
+    out["levels_collectives"] = ablmc.last_collective_count()
+    b = ablmc.LevelStats().init(3, prb.h_level(3), prb.dim())
+    ablmc.accumulate_samples(b, 11, count // 3, prb, 3)
+    out["binned"] = _key(b)
+    m = ablmc.run_mlmc(pr, 1e-3)
+    out["mlmc"] = (m.estimate, m.stat_error, [_key(s) for s in m.level_stats])
+    out["device"] = _key(_device_result(pr, 4, 3, count))
+    out["empty"] = _key(_device_result(pr, 4, 3, 0))
+    return out
+
+
+def test_init_devices_native_nccl_is_bit_identical():
+    n = torch.cuda.device_count()
+    pr = ablmc.Problem.make(ablmc.ModelParams(), ablmc.Integrator.gl, ablmc.QoISpec(), 0.05, 0.1,
+                            1.0, 2, 21)
+    q = ablmc.QoISpec(kind=ablmc.QoIKind.binned_field, bin_edges=ablmc.equidistant_edges(16, 1.0))
+    prb = ablmc.Problem.make(ablmc.ModelParams(), ablmc.Integrator.baoab, q, 0.05, 0.1, 1.0, 4, 9)
+    count = 3 * (1 << 22) + 777
+    ablmc.init(0)
+    single = _workload(pr, prb, count)
+    assert single["samples_collectives"] == 0 and single["levels_collectives"] == 0
+    try:
+        ablmc.init_devices(n)
+        info = ablmc.group_info()
+        assert info == {"mode": 3, "rank": 0, "world": n, "n_local": n}
+        grouped = _workload(pr, prb, count)
+    finally:
+        ablmc.init(0)
+    # ONE all-gather per call, and per batch of five levels
+    assert grouped["samples_collectives"] == 1 and grouped["levels_collectives"] == 1
+    for k in single:
+        if not k.endswith("collectives"):
+            assert grouped[k] == single[k], k
+    assert ablmc.group_info()["mode"] == 0
+
+
+def test_init_group_world_one_and_errors():
+    ablmc.init(0)
+    uid = ablmc.nccl_unique_id()
+    assert len(uid) == 128 and any(uid)
+    with pytest.raises(ValueError):
+        ablmc.init_group(0, 1, 1, uid)  # rank out of range
+    pr = ablmc.Problem.make(ablmc.ModelParams(), ablmc.Integrator.se, ablmc.QoISpec(), 0.5, 0.1,
+                            1.0, 1, 42)
+    one = _device_result(pr, 10, 0, 1 << 22)
+    try:
+        ablmc.init_group(0, 0, 1, uid)
+        assert ablmc.group_info()["mode"] == 2
+        grp = _device_result(pr, 10, 0, 1 << 22)
+        with pytest.raises(ValueError, match="native NCCL group"):
+            from paper_1612_07717_b200 import capi
+            ablmc._check(ablmc.lib().ablmc_set_collective(0, 1, capi.ALLGATHER_FN(lambda *a: 0), None))
+    finally:
+        ablmc.init(0)
+    assert _key(grp) == _key(one)
+    assert np.isfinite(one.mean())

@@ -35,3 +35,16 @@ def test_adapter_matches_reference_accumulate():
         assert (g_n, g_c) == (c_n, c_c)
         assert abs(g_y - c_y) <= 1e-11 * abs(c_y) + 1e-13
         assert abs(g_y2 - c_y2) <= 1e-11 * abs(c_y2)
+
+
+@needs_demo
+@pytest.mark.gpu
+def test_adapter_sharded_over_all_gpus_same_bits():
+    """The reference's C++ with init_devices(n): every accumulate call sharded
+    over the process's GPUs with one NCCL all-gather -- the same output bytes
+    as the one-GPU run."""
+    n = torch.cuda.device_count()
+    one = subprocess.run([str(DEMO), "20000"], capture_output=True, text=True, timeout=300)
+    many = subprocess.run([str(DEMO), "20000", str(n)], capture_output=True, text=True, timeout=300)
+    assert one.returncode == 0 and many.returncode == 0, many.stdout + many.stderr
+    assert many.stdout == one.stdout
