@@ -232,10 +232,14 @@ def test_binned_64_and_indicators_vs_oracle():
 
 
 @pytest.mark.parametrize("bins,delta,uneven", [(256, 0.1, True), (37, 1e-12, True),
-                                               (64, 0.3, False), (2, 0.05, False)])
+                                               (64, 0.3, False), (2, 0.05, False),
+                                               (1024, 0.1, True), (1024, 0.002, False),
+                                               (5000, 0.01, True)])
 def test_binned_field_band_reduction_vs_oracle(bins, delta, uneven):
     """K4 (banded binned field): many bins, non-equidistant edges, a delta so
-    small the band is disabled, a wide band, and a 2-bin field."""
+    small the band is disabled, a wide band, a 2-bin field, and fields wider
+    than the old 256-bin cap (bin groups streamed through shared memory; 5000
+    bins: edges read from global memory)."""
     rng = np.random.default_rng(bins)
     if uneven:
         inner = np.sort(rng.uniform(0.0, 1.0, bins - 1))

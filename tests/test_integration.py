@@ -47,4 +47,10 @@ def test_adapter_sharded_over_all_gpus_same_bits():
     one = subprocess.run([str(DEMO), "20000"], capture_output=True, text=True, timeout=300)
     many = subprocess.run([str(DEMO), "20000", str(n)], capture_output=True, text=True, timeout=300)
     assert one.returncode == 0 and many.returncode == 0, many.stdout + many.stderr
-    assert many.stdout == one.stdout
+    # (this image sets NCCL_DEBUG=VERSION: NCCL's own version line goes to
+    # stdout of the multi-device run; compare the demo's output lines)
+    def levels(out):
+        return [l for l in out.splitlines() if l.startswith("level")]
+
+    assert len(levels(one.stdout)) == 4
+    assert levels(many.stdout) == levels(one.stdout)
