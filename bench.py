@@ -227,7 +227,12 @@ class ClockSampler:
 
 
 # ------------------------------------------------------- extra measurements
-def per_integrator(a, lib, stream, peak):
+def _k1_profile() -> dict:
+    tp = ROOT / "profiles" / "k1_ncu.json"
+    return json.loads(tp.read_text()) if tp.exists() else {}
+
+
+def per_integrator(a, lib, stream, peak, clock_hz=None):
     """Level-10 coupled throughput of all three integrators (2^23 paths, one
     warm-up + 2 timed accumulate calls each, CUDA events on the stream)."""
     import torch
@@ -245,8 +250,11 @@ def per_integrator(a, lib, stream, peak):
         e.record(stream)
         torch.cuda.synchronize()
         rate = 2 * n * (1 << a.level) / (s.elapsed_time(e) * 1e-3)
-        out[IG_NAME[ig]] = {"path_steps_per_s": rate, "W_alg": W_ALG[ig],
-                            "roofline_frac": rate * W_ALG[ig] / peak, "paths": n}
+        w_exec = _k1_profile().get(IG_NAME[ig], {}).get("fp64_instr_per_path_step")
+        out[IG_NAME[ig]] = {"path_steps_per_s": rate, "W_executed_ncu": w_exec,
+                            "roofline_frac": rate * w_exec / peak if w_exec else None,
+                            "W_alg": W_ALG[ig], "roofline_frac_W_alg": rate * W_ALG[ig] / peak,
+                            "paths": n}
     # fp32-state variant (BASELINE config 5; statistical parity only)
     from paper_1612_07717_b200 import ablmc
     for ig in (0, 1, 2):
@@ -261,8 +269,24 @@ def per_integrator(a, lib, stream, peak):
             lib.ablmc_accumulate_device(pc, a.level, 0, n)
         e.record(stream)
         torch.cuda.synchronize()
-        out[IG_NAME[ig] + "_fp32_state"] = {"path_steps_per_s": 2 * n * (1 << a.level) /
-                                            (s.elapsed_time(e) * 1e-3), "paths": n}
+        rate = 2 * n * (1 << a.level) / (s.elapsed_time(e) * 1e-3)
+        row = {"path_steps_per_s": rate, "paths": n}
+        # W32 roofline: FP32-pipe arithmetic instructions per
+        # path-step (ncu, profiles/k1_ncu.json) against the 128-lane FFMA pipe
+        # at the SM clock of this run; the variant is issue-bound, so the issue
+        # fraction (all instructions / 4 SMSPs x 1 warp-instr per cycle) and
+        # the MUFU (XU) count are reported beside it
+        prof = _k1_profile().get(IG_NAME[ig] + "_fp32_state")
+        if prof and clock_hz:
+            w32, ins = prof["fp32_instr_per_path_step"], prof["instr_per_path_step"]
+            row.update({"W32_fp32_pipe": w32, "mufu_per_path_step": prof["mufu_per_path_step"],
+                        "instr_per_path_step": ins,
+                        "roofline_frac_fp32_pipe": rate * w32 / (148 * 128 * clock_hz),
+                        "issue_frac": rate * ins / 32 / (148 * 4 * clock_hz),
+                        "ncu_pct": {k: prof[k] for k in ("issue_active_pct", "fma_pipe_pct",
+                                                          "alu_pipe_pct", "xu_pipe_pct")},
+                        "source": prof["source"]})
+        out[IG_NAME[ig] + "_fp32_state"] = row
     out["adaptive"] = adaptive_rates(lib, stream)
     return out
 
@@ -618,7 +642,9 @@ def run_b200(a):
         "estimate": {"mean_y": acc.mean(), "n": acc.n, "failed": acc.failed},
     }
     if not a.no_extras and world == 1:
-        line["per_integrator"] = per_integrator(a, lib, stream, fp64_rate.value)
+        sm = clk.summary()["sm_mhz"]
+        line["per_integrator"] = per_integrator(a, lib, stream, fp64_rate.value,
+                                                sm * 1e6 if sm else None)
         line["mlmc_time_to_eps"] = mlmc_sweep(a)
         line["baseline_configs"] = configs_sweep(lib, stream)
     if not a.no_cpu_baseline and world == 1:

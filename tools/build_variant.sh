@@ -17,7 +17,8 @@ $NV "$@" -Xptxas -v -c "$csrc/adaptive_kernels.cu" -o "/tmp/ak_$name.o" 2>>"/tmp
 $NV "$@" -c "$csrc/binned_kernels.cu" -o "/tmp/bk_$name.o"
 $NV "$@" -c "$csrc/capi.cu" -o "/tmp/capi_$name.o"
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$out/lib_$name.so" "/tmp/lk_$name.o" \
-  "/tmp/ak_$name.o" "/tmp/bk_$name.o" "/tmp/capi_$name.o" "$obj/drivers.o" "$obj/output.o" \
+  "/tmp/ak_$name.o" "/tmp/bk_$name.o" "/tmp/capi_$name.o" "$obj/collective.o" "$obj/drivers.o" \
+  "$obj/output.o" \
   -cudart static
 awk '/Compiling entry/ {n=$0} /Used|spill/ {print n; print $0}' "/tmp/ptx_$name.txt" \
   | grep -A1 "k_levelILi[012]ELi0ELb1ELb0" | grep -E "Used" | sed "s/^/$name /"

@@ -52,5 +52,8 @@ total = sum(cnt.values())
 print(f"dynamic SASS per coupled fine path-step (thread instructions), total {total * 32 / path_steps:.1f}:")
 fp64 = sum(cnt[o] for o in ("DFMA", "DMUL", "DADD", "DSETP", "DMNMX")) * 32 / path_steps
 print(f"  FP64-pipe (DFMA+DMUL+DADD+DSETP+DMNMX): {fp64:.1f}")
+fp32 = sum(cnt[o] for o in ("FFMA", "FMUL", "FADD", "FSETP", "FMNMX", "FSWZADD")) * 32 / path_steps
+print(f"  FP32 arithmetic (FFMA+FMUL+FADD+FSETP+FMNMX): {fp32:.1f}")
+print(f"  MUFU (XU): {cnt['MUFU'] * 32 / path_steps:.1f}")
 for op, n in cnt.most_common(24):
     print(f"  {op:8s} {n * 32 / path_steps:7.2f}")
