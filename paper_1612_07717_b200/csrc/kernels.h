@@ -24,6 +24,14 @@ constexpr int kCnt = 3;
 #ifndef ABLMC_MINB_PATH
 #define ABLMC_MINB_PATH 5
 #endif
+// samples per thread of the short-path (level 0 / StMC, M <= 4) kernel and
+// the unroll of its per-thread sample loop
+#ifndef ABLMC_SPT_SHORT
+#define ABLMC_SPT_SHORT 4
+#endif
+#ifndef ABLMC_SPT_UNROLL
+#define ABLMC_SPT_UNROLL 1
+#endif
 #ifndef ABLMC_MINB_BAOAB
 #define ABLMC_MINB_BAOAB 3
 #endif

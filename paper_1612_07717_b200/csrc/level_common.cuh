@@ -402,13 +402,17 @@ __device__ __forceinline__ void tile_prologue() {
 // in tile order, the last block of a 2^22-sample super-block sums the block
 // partials in the segment order of seg_fold -- the fixed orders of merge_tail
 // below.
+// SPT: samples per thread of the launch (a tile covers SPT * kTile samples,
+// a 4096-sample block ABLMC_TILES_PER_BLOCK / SPT tiles).
+template <int SPT = 1>
 __device__ __forceinline__ void merge_tail_warp(const KernelArgs& a, const double* tile_sums,
                                                 const long long* tile_cnt, int dim2) {
+  constexpr int kTpb = ABLMC_TILES_PER_BLOCK / SPT;
   const int lane = threadIdx.x & 31;
-  const int64_t n_tiles = (a.n + kTile - 1) / kTile;
-  const int64_t blk = blockIdx.x / ABLMC_TILES_PER_BLOCK;
-  const int64_t t0 = blk * ABLMC_TILES_PER_BLOCK;
-  const int64_t t1 = min(t0 + int64_t(ABLMC_TILES_PER_BLOCK), n_tiles);
+  const int64_t n_tiles = (a.n + SPT * kTile - 1) / (SPT * kTile);
+  const int64_t blk = blockIdx.x / kTpb;
+  const int64_t t0 = blk * kTpb;
+  const int64_t t1 = min(t0 + int64_t(kTpb), n_tiles);
   unsigned last = 0;
   if (lane == 0) {
     __threadfence();  // lane 0 wrote this tile's partial
@@ -424,7 +428,7 @@ __device__ __forceinline__ void merge_tail_warp(const KernelArgs& a, const doubl
   }
   __threadfence();
   __syncwarp();
-  const int64_t n_blk = (n_tiles + ABLMC_TILES_PER_BLOCK - 1) / ABLMC_TILES_PER_BLOCK;
+  const int64_t n_blk = (n_tiles + kTpb - 1) / kTpb;
   const int64_t sb = blk / ABLMC_BLOCKS_PER_SUPER;
   const int64_t b0 = sb * ABLMC_BLOCKS_PER_SUPER;
   const int64_t b1 = min(b0 + int64_t(ABLMC_BLOCKS_PER_SUPER), n_blk);
@@ -460,34 +464,19 @@ __device__ __forceinline__ void merge_tail_warp(const KernelArgs& a, const doubl
 // UNIFORM_STEPS: every successful sample of the tile took `steps` steps (the
 // uniform grids), so the counts are two warp votes; otherwise (adaptive) the
 // step counts are summed by shuffles.  Integer sums: the same values either way.
-template <bool UNIFORM_STEPS>
-__device__ __forceinline__ void tile_reduce(const KernelArgs& a, bool active, bool good, double y,
-                                            long long steps, bool binned,
-                                            double* __restrict__ tile_sums,
-                                            long long* __restrict__ tile_cnt) {
+// The common tail: per-thread sums (sy, sy2) of the thread's successful
+// samples and the warp's counts (cn, cf, cc: warp totals, identical in every
+// lane) -> fixed warp-shuffle tree -> warps in order (last warp to arrive)
+// -> tile partial at tile blockIdx.x -> block / super-block merge.
+template <int SPT = 1>
+__device__ __forceinline__ void tile_reduce_sums(const KernelArgs& a, double sy, double sy2,
+                                                 long long cn, long long cf, long long cc,
+                                                 bool binned, double* __restrict__ tile_sums,
+                                                 long long* __restrict__ tile_cnt) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ double s_red[kWarps][2];
   __shared__ long long s_cnt[kWarps][kCnt];
-  long long cn, cf, cc;
-  if (UNIFORM_STEPS) {
-    cn = __popc(__ballot_sync(0xffffffffu, good));
-    cf = __popc(__ballot_sync(0xffffffffu, active && !good));
-    cc = cn * steps;
-  } else {
-    cn = good ? 1 : 0;
-    cf = (active && !good) ? 1 : 0;
-    cc = good ? steps : 0;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      cn += __shfl_down_sync(0xffffffffu, cn, off);
-      cf += __shfl_down_sync(0xffffffffu, cf, off);
-      cc += __shfl_down_sync(0xffffffffu, cc, off);
-    }
-  }
-  double sy = 0.0, sy2 = 0.0;
   if (!binned) {
-    sy = good ? y : 0.0;
-    sy2 = good ? mul(y, y) : 0.0;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
       sy = add(sy, __shfl_down_sync(0xffffffffu, sy, off));
@@ -523,7 +512,45 @@ __device__ __forceinline__ void tile_reduce(const KernelArgs& a, bool active, bo
     }
     for (int c = 0; c < kCnt; ++c) tile_cnt[kCnt * blockIdx.x + c] = t[c];
   }
-  if (!binned) merge_tail_warp(a, tile_sums, tile_cnt, 2);
+  if (!binned) merge_tail_warp<SPT>(a, tile_sums, tile_cnt, 2);
+}
+
+// Tile reduction shared by the level kernels: the tile's {sum_y, sum_y2}
+// (fixed warp-shuffle tree, then warps in order) of the successful samples'
+// QoI values y, and counts {n, failed, cost_steps}.  Binned field: sums come
+// from K4, only the counts are reduced here.  No CTA barrier: each warp
+// leaves its partial in shared memory and the LAST warp to arrive (shared
+// arrival counter, zeroed by tile_prologue) sums the warps in order, writes
+// the tile partial and, for scalar QoIs, runs the block/super-block merge;
+// the other warps retire at once (at level 0 the barrier was 27% of the
+// stalls).
+// UNIFORM_STEPS: every successful sample of the tile took `steps` steps (the
+// uniform grids), so the counts are two warp votes; otherwise (adaptive) the
+// step counts are summed by shuffles.  Integer sums: the same values either way.
+template <bool UNIFORM_STEPS>
+__device__ __forceinline__ void tile_reduce(const KernelArgs& a, bool active, bool good, double y,
+                                            long long steps, bool binned,
+                                            double* __restrict__ tile_sums,
+                                            long long* __restrict__ tile_cnt) {
+  long long cn, cf, cc;
+  if (UNIFORM_STEPS) {
+    cn = __popc(__ballot_sync(0xffffffffu, good));
+    cf = __popc(__ballot_sync(0xffffffffu, active && !good));
+    cc = cn * steps;
+  } else {
+    cn = good ? 1 : 0;
+    cf = (active && !good) ? 1 : 0;
+    cc = good ? steps : 0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      cn += __shfl_down_sync(0xffffffffu, cn, off);
+      cf += __shfl_down_sync(0xffffffffu, cf, off);
+      cc += __shfl_down_sync(0xffffffffu, cc, off);
+    }
+  }
+  const double sy = (!binned && good) ? y : 0.0;
+  const double sy2 = (!binned && good) ? mul(y, y) : 0.0;
+  tile_reduce_sums<1>(a, sy, sy2, cn, cf, cc, binned, tile_sums, tile_cnt);
 }
 
 // Single-pass merge, run by every CTA after its tile partial is written:

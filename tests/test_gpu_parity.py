@@ -276,22 +276,41 @@ def test_deterministic_and_add_merge():
     assert abs(c.sum_y[0] - a.sum_y[0]) <= 1e-12 * abs(a.sum_y[0])
 
 
-def test_superblock_sharding_is_bit_identical():
-    pr = ablmc.Problem.make(ablmc.ModelParams(), Ig.gl, ablmc.QoISpec(), 0.05, 0.1, 1.0, 2, 21)
+@pytest.mark.parametrize("level,m0", [(1, 2), (0, 1), (0, 4)])  # level 0, M <= 4: 4 samples/thread
+def test_superblock_sharding_is_bit_identical(level, m0):
+    pr = ablmc.Problem.make(ablmc.ModelParams(), Ig.gl, ablmc.QoISpec(), 0.05, 0.1, 1.0, m0, 21)
     count = 3 * capi.ABLMC_SUPERBLOCK + 12345  # ragged last super-block
-    one = ablmc.LevelStats().init(1, pr.h_level(1), 1)
-    ablmc.accumulate_samples(one, 17, count, pr, 1)
+    one = ablmc.LevelStats().init(level, pr.h_level(level), 1)
+    ablmc.accumulate_samples(one, 17, count, pr, level)
     nsb = ablmc.num_superblocks(count)
     assert nsb == 4
     for split in ([0, 4], [0, 1, 4], [0, 2, 3, 4], [0, 1, 2, 3, 4]):
-        parts = [ablmc.accumulate_partials(pr, 1, 17, count, lo, hi)
+        parts = [ablmc.accumulate_partials(pr, level, 17, count, lo, hi)
                  for lo, hi in zip(split[:-1], split[1:])]
         sums = np.concatenate([p[0] for p in parts])
         cnts = np.concatenate([p[1] for p in parts])
-        acc = ablmc.LevelStats().init(1, pr.h_level(1), 1)
-        ablmc.merge_partials(acc, pr, 1, sums, cnts)
+        acc = ablmc.LevelStats().init(level, pr.h_level(level), 1)
+        ablmc.merge_partials(acc, pr, level, sums, cnts)
         assert acc.sum_y[0] == one.sum_y[0] and acc.sum_y2[0] == one.sum_y2[0]
         assert (acc.n, acc.failed, acc.cost_steps) == (one.n, one.failed, one.cost_steps)
+
+
+@pytest.mark.parametrize("ig", list(Ig))
+@pytest.mark.parametrize("count,first", [(1, 0), (255, 3), (1023, 1), (1025, 4096 - 7), (70001, 11)])
+def test_short_path_tiles_vs_oracle(ig, count, first):
+    """Level 0 with M <= 4 runs 4 samples per thread (1024-sample tiles):
+    ragged counts and offsets, every integrator, sums vs the oracle and counts
+    exact (accumulate_samples, stats.hpp:96-136; level0_sample,
+    coupling.hpp:228-244)."""
+    for m0, u0 in ((1, 0.1), (3, 0.0), (4, 0.1)):
+        pr = ablmc.Problem.make(ablmc.ModelParams(), ig, ablmc.QoISpec(), 0.05, u0, 1.0, m0, 5)
+        acc = ablmc.LevelStats().init(0, pr.h_level(0), 1)
+        ablmc.accumulate_samples(acc, first, count, pr, 0)
+        ref = O.Stats(1)
+        assert O.orc().orc_accumulate_samples(C.byref(pr._c), 0, first, count, C.byref(ref.c)) == 0
+        assert (acc.n, acc.failed, acc.cost_steps) == (ref.n, ref.failed, ref.cost_steps)
+        assert close(acc.sum_y, ref.sum_y, 1e-12, 1e-15)
+        assert close(acc.sum_y2, ref.sum_y2, 1e-12, 1e-15)
 
 
 def test_device_resident_result_matches_host_path():
