@@ -43,6 +43,54 @@ struct SeqNoise {
   }
 };
 
+// The persistent sampler's stream (the same draws in the same order as
+// SeqNoise): up to three upcoming normals per lane, refilled one Philox block
+// (two normals) at a time in warp-wide batches.  Lanes sit at different
+// draws of different samples, so a block generated on demand (SeqNoise: at
+// every even draw) ran Philox + Box-Muller on ~44% of the lanes nearly every
+// event; here a refill runs only when some lane's buffer is empty, and then
+// for every lane holding at most kRefillAt normals (refill_if_any_empty).
+#ifndef ABLMC_BUF_NORMALS
+#define ABLMC_BUF_NORMALS 3  // buffer capacity: 3 (refill at <= 1) or 4 (refill at <= 2)
+#endif
+struct BufNoise {
+  uint64_t blk;  // next Philox block of the sample's stream
+  double q0, q1, q2, q3;
+  int n;         // normals buffered (q0 is the next draw)
+  static constexpr int kRefillAt = ABLMC_BUF_NORMALS - 2;
+  __device__ __forceinline__ void reset() {
+    blk = 0;
+    n = 0;
+  }
+  template <class Key>
+  __device__ __forceinline__ void refill(uint64_t idx, const Key& key) {  // n <= kRefillAt
+    double z0, z1;
+    normal_pair(blk, idx, key, z0, z1);
+    ++blk;
+    if (ABLMC_BUF_NORMALS == 4) q3 = n == 2 ? z1 : q3;
+    q2 = n == 1 ? z1 : (n == 2 ? z0 : q2);
+    q1 = n == 0 ? z1 : (n == 1 ? z0 : q1);
+    q0 = n == 0 ? z0 : q0;
+    n += 2;
+  }
+  template <class Key>
+  __device__ __forceinline__ double next(uint64_t, const Key&) {  // n >= 1
+    const double z = q0;
+    q0 = q1;
+    q1 = q2;
+    if (ABLMC_BUF_NORMALS == 4) q2 = q3;
+    --n;
+    return z;
+  }
+};
+// Warp-uniform point of the persistent loop (at most one draw per event).
+template <class Key>
+__device__ __forceinline__ void refill_if_any_empty(BufNoise& ns, bool live, uint64_t idx,
+                                                    const Key& key) {
+  if (__any_sync(__activemask(), live && ns.n == 0) && live && ns.n <= BufNoise::kRefillAt)
+    ns.refill(idx, key);
+}
+
 // timeline.hpp:18-23 — min{h, lambda(x_adapt)/lambda(x) h}
 template <int FAST>
 __device__ __forceinline__ double adaptive_h(double lam_x, double h, double lam_ref, bool& bad) {
@@ -384,7 +432,7 @@ struct PairSM {
   LegHot f, c;
   double t, tau;
   long long iter;
-  SeqNoise<PhiloxKey> ns;
+  BufNoise ns;
   bool pend_c;
 };
 
@@ -506,7 +554,7 @@ struct PathSM {
   Coef c;
   double t;
   long long steps;
-  SeqNoise<PhiloxKey> ns;
+  BufNoise ns;
 };
 
 // One step of simulate_path_adaptive (coupling.hpp:41-49).
@@ -536,11 +584,15 @@ __device__ __forceinline__ bool path_event(PathSM& S, const KernelArgs& a, uint6
   return !ok || !(S.t < T) || (FAST && bad);
 }
 
-template <int IG, int PROF, bool COUPLED, int FAST>
 #ifndef ABLMC_MINB_ADAPTIVE
-#define ABLMC_MINB_ADAPTIVE 2  // 128 registers, no spills: 2 CTAs/SM (3 spills and is slower)
+#define ABLMC_MINB_ADAPTIVE 2  // 2 CTAs/SM (<= 128 registers, no spills)
 #endif
-__global__ void __launch_bounds__(kTile, ABLMC_MINB_ADAPTIVE) k_adaptive_persistent(const KernelArgs a) {
+#ifndef ABLMC_MINB_ADAPTIVE_SE
+#define ABLMC_MINB_ADAPTIVE_SE ABLMC_MINB_ADAPTIVE
+#endif
+template <int IG, int PROF, bool COUPLED, int FAST>
+__global__ void __launch_bounds__(kTile, IG == kSE ? ABLMC_MINB_ADAPTIVE_SE : ABLMC_MINB_ADAPTIVE)
+    k_adaptive_persistent(const KernelArgs a) {
   const DevModel& m = a.model;
   bool bad = false;
   const double lam_ref = coeffs<PROF, FAST>(a.x_adapt, m, bad).lam;
@@ -573,14 +625,14 @@ __global__ void __launch_bounds__(kTile, ABLMC_MINB_ADAPTIVE) k_adaptive_persist
       P.c = leg_hot(c0);
       P.t = 0.0;
       P.iter = 0;
-      P.ns.k = 0;
+      P.ns.reset();
       P.pend_c = false;
     } else {
       Q.s = f0.s;
       Q.c = f0.c;
       Q.t = 0.0;
       Q.steps = 0;
-      Q.ns.k = 0;
+      Q.ns.reset();
     }
     bad = bad0;
     deep = false;
@@ -589,6 +641,7 @@ __global__ void __launch_bounds__(kTile, ABLMC_MINB_ADAPTIVE) k_adaptive_persist
   if (j < a.n) start();
   while (j < a.n) {
     const uint64_t idx = uint64_t(a.first + a.offset + j);
+    refill_if_any_empty(COUPLED ? P.ns : Q.ns, true, idx, a.key);
     bool ok = true;
     const bool fin = COUPLED ? pair_event<IG, PROF, FAST>(P, st, sp, a, idx, lam_ref, ok, bad, deep)
                              : path_event<IG, PROF, FAST>(Q, a, idx, lam_ref, ok, bad);
