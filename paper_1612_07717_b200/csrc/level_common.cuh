@@ -53,6 +53,42 @@ __device__ __forceinline__ bool first_step_finish(PState& s, const FirstStep& F,
   return true;
 }
 
+// Level-0 sample of one step (simulate_path with M = 1 from the fixed
+// release state, coupling.hpp:22-29 / 228-244) on the FAST path, for QoIs
+// that read the position only: the draw is the cosine half of Philox block 0
+// (noise.hpp:60-75; z1 is never used), the step is first_step_finish's with
+// the sample-independent part hoisted on the host, and BAOAB's closing B
+// half-kick, which changes only the velocity and cannot fail, is skipped.
+// Returns x_T; `bad` as in run_sample (the caller recomputes the sample with
+// the general path).
+template <int IG, int PROF>
+__device__ __forceinline__ double level0_x(const KernelArgs& a, uint64_t idx, const Coef& cx0,
+                                           bool& bad) {
+  uint32_t w[4];
+  philox4x32(0u, 0u, uint32_t(idx), uint32_t(idx >> 32), a.key, w);
+  double z0, z1;
+  box_muller<true>(unit_2p54(w[0], w[1]), unit_2p54(w[2], w[3]), z0, z1);
+  (void)z1;
+  const FirstStep& F = a.fs[0];
+  const DevModel& m = a.model;
+  PState s;
+  if (IG == kSE) {
+    s = {a.x0, a.u0, 1, 0};
+    const double u1 = add(F.AB, mul(F.G, z0));
+    reflect_fast(s, add(s.x, mul(u1, a.h)), u1, m, bad);
+  } else if (IG == kGL) {
+    s = {a.x0, a.u0, 1, 0};
+    const double us = add(F.D, mul(F.G, z0));
+    const double u1 = sub(us, mul(dv_dx<kFastUnit>(cx0, us, bad), a.h));
+    reflect_fast(s, add(s.x, mul(u1, a.h)), u1, m, bad);
+  } else {
+    s = {F.x, F.u, F.par, F.nrefl};
+    const double us = add(F.D, mul(F.G, z0));
+    reflect_fast(s, add(s.x, mul(us, a.h_half)), us, m, bad);
+  }
+  return s.x;
+}
+
 // simulate_pair (coupling.hpp:64-105) / simulate_path (coupling.hpp:22-29)
 // for one sample.  XI: read normals from xi (oracle mode) instead of Philox.
 // FAST: fast div/sqrt; returns early with bad = true on any fast-path miss
