@@ -428,10 +428,13 @@ def mlmc_sweep(a):
     res = {}
     pr = problem_c(2)
     for eps in [float(e) for e in a.mlmc_eps.split(",") if e]:
-        t0 = time.perf_counter()
-        r = ablmc.run_mlmc(pr, eps)
-        t = time.perf_counter() - t0
-        row = {"seconds": t, "estimate": r.estimate[0], "stat_error": r.stat_error[0],
+        times = []
+        for _ in range(3):  # best of 3 (host-side wall clock of the whole driver)
+            t0 = time.perf_counter()
+            r = ablmc.run_mlmc(pr, eps)
+            times.append(time.perf_counter() - t0)
+        t = min(times)
+        row = {"seconds": t, "seconds_all": times, "estimate": r.estimate[0], "stat_error": r.stat_error[0],
                "bias_estimate": r.bias_estimate, "levels": r.levels_used,
                "N_l": [st.n for st in r.level_stats], "total_cost_steps": r.total_cost_steps,
                "eps_m": eps * 1000.0}

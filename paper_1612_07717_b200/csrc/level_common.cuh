@@ -93,7 +93,9 @@ __device__ __forceinline__ double level0_x(const KernelArgs& a, uint64_t idx, co
 // for one sample.  XI: read normals from xi (oracle mode) instead of Philox.
 // FAST: fast div/sqrt; returns early with bad = true on any fast-path miss
 // (the caller then recomputes the sample with FAST = false).
-template <int IG, int PROF, bool COUPLED, bool XI, int FAST>
+// SHORT (coupled only): the caller guarantees M == 2 (one window); only that
+// path is compiled (the short-path kernel).
+template <int IG, int PROF, bool COUPLED, bool XI, int FAST, bool SHORT = false>
 __device__ __forceinline__ PathOut run_sample(const KernelArgs& a, uint64_t idx,
                                               const double* __restrict__ xi, bool& bad) {
   const DevModel& m = a.model;
@@ -274,6 +276,12 @@ __device__ __forceinline__ PathOut run_sample(const KernelArgs& a, uint64_t idx,
     }
     return ok;
   };
+  if constexpr (SHORT) {  // M = 2: the same branches as below for windows == 1
+    if (a.fs_ok) o.ok = window0_hoisted();
+    else if (IG != kBAOAB) o.ok = window(std::true_type{}, 0);
+    else o.ok = window(std::false_type{}, 0);
+    return o;
+  }
   constexpr bool kPeelMore = IG != kSE && PROF == kProfileReference;
   if (a.fs_ok && windows == 1) {  // M = 2: the whole sample
     o.ok = window0_hoisted();
@@ -303,17 +311,18 @@ __device__ __forceinline__ PathOut run_sample(const KernelArgs& a, uint64_t idx,
 // One sample with IEEE-exact div/sqrt semantics: the fast variant when the
 // host certified tame parameters, recomputed with the IEEE variant on a
 // fast-path miss.
-template <int IG, int PROF, bool COUPLED, bool XI>
+template <int IG, int PROF, bool COUPLED, bool XI, bool SHORT = false>
 __device__ __forceinline__ PathOut sample(const KernelArgs& a, uint64_t idx,
                                           const double* __restrict__ xi) {
   bool bad = false;
   if (a.fast) {
-    PathOut o = a.fast == kFastUnit ? run_sample<IG, PROF, COUPLED, XI, kFastUnit>(a, idx, xi, bad)
-                                    : run_sample<IG, PROF, COUPLED, XI, 1>(a, idx, xi, bad);
+    PathOut o = a.fast == kFastUnit
+                    ? run_sample<IG, PROF, COUPLED, XI, kFastUnit, SHORT>(a, idx, xi, bad)
+                    : run_sample<IG, PROF, COUPLED, XI, 1, SHORT>(a, idx, xi, bad);
     if (!bad) return o;
     bad = false;
   }
-  return run_sample<IG, PROF, COUPLED, XI, 0>(a, idx, xi, bad);
+  return run_sample<IG, PROF, COUPLED, XI, 0, SHORT>(a, idx, xi, bad);
 }
 
 // ----------------------------------------------------------------- QoI

@@ -313,6 +313,27 @@ def test_short_path_tiles_vs_oracle(ig, count, first):
         assert close(acc.sum_y2, ref.sum_y2, 1e-12, 1e-15)
 
 
+@pytest.mark.parametrize("level,m0,first", [(0, 1, 2**32 - 1000), (2, 4, 2**32 - 1000),
+                                            (1, 2, 2**40 + 17)])
+def test_sample_indices_above_32_bits_vs_oracle(level, m0, first):
+    """Index ranges crossing 2^32 and beyond 2^40 (the Philox counter's idx
+    high word, noise.hpp:63-70): sums vs the oracle, device normals vs the
+    oracle's stream."""
+    for ig in Ig:
+        pr = ablmc.Problem.make(ablmc.ModelParams(), ig, ablmc.QoISpec(), 0.05, 0.1, 1.0, m0, 9)
+        acc = ablmc.LevelStats().init(level, pr.h_level(level), 1)
+        ablmc.accumulate_samples(acc, first, 3000, pr, level)
+        ref = O.Stats(1)
+        assert O.orc().orc_accumulate_samples(C.byref(pr._c), level, first, 3000, C.byref(ref.c)) == 0
+        assert (acc.n, acc.failed, acc.cost_steps) == (ref.n, ref.failed, ref.cost_steps)
+        assert close(acc.sum_y, ref.sum_y, 1e-12, 1e-15)
+        assert close(acc.sum_y2, ref.sum_y2, 1e-12, 1e-15)
+    for idx in (2**32 - 1, 2**32, 2**40 + 3):
+        z = ablmc.normals(9, level, idx, 0, 8)
+        want = O.orc_normals(9, level, idx, 0, 8)
+        assert np.all(np.abs(z - want) <= 1e-13 * np.abs(want) + 1e-15)
+
+
 def test_device_resident_result_matches_host_path():
     pr = ablmc.Problem.make(ablmc.ModelParams(), Ig.se, ablmc.QoISpec(), 0.5, 0.1, 1.0, 1, 42)
     lib = ablmc.lib()

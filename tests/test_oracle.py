@@ -142,6 +142,19 @@ def test_normals_bit_exact(ref_vectors):
         assert [v.hex() for v in z] == s["z"]
 
 
+@pytest.mark.parametrize("idx,k0", [(2**32 - 1, 0), (2**32, 6), (2**40 + 3, 1), (2**63 + 5, 2),
+                                    (12345, 2**33 - 2), (7, 2**33 + 1)])
+def test_normals_bit_exact_high_counter_words(idx, k0):
+    """Sample indices and draw numbers whose Philox counter words above 32
+    bits are nonzero (noise.hpp:63-70: ctr = (k>>1, k>>33, idx, idx>>32)),
+    live against the reference itself (oracle/_ref)."""
+    if O.ref() is None:
+        pytest.skip("oracle/_ref not built")
+    z = O.orc_normals(42, 3, idx, k0, 6)
+    r = O.ref_normals(42, 3, idx, k0, 6)
+    assert [v.hex() for v in z] == [v.hex() for v in r]
+
+
 def test_sde_coeffs_bit_exact(ref_vectors):
     p = O.default_params()
     for e in ref_vectors["sde_coeffs"]:
