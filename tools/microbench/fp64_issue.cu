@@ -47,6 +47,8 @@ __global__ void __launch_bounds__(256, 4) mix(double* out, long long* cyc, int i
         else if (KIND == 4) d[k] = d[k] * x[k];
         else if (KIND == 10) d[k] = fma(d[k], x[k], 1e-7);  // 2 register operands + constant
         else if (KIND == 11) {}  // integer only
+        else if (KIND == 13) d[k] = fma(d[k], d[k], d[k]) * 0.5;  // one register three times (+DMUL imm)
+        else if (KIND == 14) d[k] = fma(d[k], x[k], 0.5);  // 2 registers + immediate
         else if (KIND == 12) {  // IMAD.WIDE only
           const unsigned long long p = (unsigned long long)u[k] * 0xD2511F53u;
           u[k] = unsigned(p >> 32) ^ unsigned(p);
@@ -133,6 +135,8 @@ int main() {
   run<10, 2>("DFMA 2-reg+const", 8, 8);
   run<10, 4>("DFMA 2-reg+const", 8, 8);
   run<12, 4>("IMAD.WIDE + LOP3 only", 16, 0);
+  run<13, 4>("DFMA(d,d,d) + DMUL imm", 16, 16);
+  run<14, 4>("DFMA 2-reg + imm", 8, 8);
   run<3, 1>("8 DFMA + MUFU.RSQ64H + DFMA", 10, 9);
   run<3, 2>("8 DFMA + MUFU.RSQ64H + DFMA", 10, 9);
   run<3, 4>("8 DFMA + MUFU.RSQ64H + DFMA", 10, 9);
