@@ -221,14 +221,17 @@ def test_extension_profiles_oracle_mode_vs_oracle(prof, ig):
 
 
 @pytest.mark.parametrize("prof", ["reference", "constant", "floored"])
-@pytest.mark.parametrize("level", [0, 2])
-def test_random_u0_and_profiles_accumulate_vs_oracle(prof, level):
+@pytest.mark.parametrize("level,m0,ig", [(0, 8, Ig.gl), (2, 8, Ig.gl),
+                                         # the short-path kernels (M = 1, 4 single; M = 2 pairs)
+                                         (0, 1, Ig.se), (0, 4, Ig.baoab), (1, 1, Ig.gl),
+                                         (1, 1, Ig.baoab), (1, 1, Ig.se)])
+def test_random_u0_and_profiles_accumulate_vs_oracle(prof, level, m0, ig):
     """D2 (w0 ~ N(0, sigma_U(x0)^2) from draw k = M of the sample's stream)
     with each profile: level sums against the oracle's accumulate on the same
     Philox streams (Box-Muller within ulps of glibc): counts and cost exact,
     sums within rel 1e-10."""
     kw = EXT.get(prof, {})
-    pr = ablmc.Problem.make(ablmc.ModelParams(), Ig.gl, ablmc.QoISpec(), 0.5, 0.0, 1.0, 8, 11,
+    pr = ablmc.Problem.make(ablmc.ModelParams(), ig, ablmc.QoISpec(), 0.5, 0.0, 1.0, m0, 11,
                             random_u0=True, **kw)
     acc = ablmc.LevelStats().init(level, pr.h_level(level), 1)
     ablmc.accumulate_samples(acc, 5, 20000, pr, level)

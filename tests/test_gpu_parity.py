@@ -313,6 +313,25 @@ def test_short_path_tiles_vs_oracle(ig, count, first):
         assert close(acc.sum_y2, ref.sum_y2, 1e-12, 1e-15)
 
 
+@pytest.mark.parametrize("signs", [True, False])
+@pytest.mark.parametrize("x0", [0.05, 0.5, 0.995])
+def test_short_coupled_pairs_vs_oracle(signs, x0):
+    """Coupled pairs of M = 2 fine steps (2 samples per thread, the one-window
+    path only): near-ground and near-ceiling releases (SE failures, first-step
+    reflections), coupling signs on/off, every integrator: counts exact
+    (failed samples excluded, coupling.hpp:262-268), sums vs the oracle."""
+    for ig in Ig:
+        pr = ablmc.Problem.make(ablmc.ModelParams(), ig, ablmc.QoISpec(), x0, 0.1, 1.0, 1, 23,
+                                ablmc.SampleOptions(signs_on=signs))
+        acc = ablmc.LevelStats().init(1, pr.h_level(1), 1)
+        ablmc.accumulate_samples(acc, 3, 20000, pr, 1)
+        ref = O.Stats(1)
+        assert O.orc().orc_accumulate_samples(C.byref(pr._c), 1, 3, 20000, C.byref(ref.c)) == 0
+        assert (acc.n, acc.failed, acc.cost_steps) == (ref.n, ref.failed, ref.cost_steps), ig
+        assert close(acc.sum_y, ref.sum_y, 1e-11, 1e-14)
+        assert close(acc.sum_y2, ref.sum_y2, 1e-11, 1e-14)
+
+
 @pytest.mark.parametrize("level,m0,first", [(0, 1, 2**32 - 1000), (2, 4, 2**32 - 1000),
                                             (1, 2, 2**40 + 17)])
 def test_sample_indices_above_32_bits_vs_oracle(level, m0, first):
