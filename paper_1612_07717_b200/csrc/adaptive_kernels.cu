@@ -417,11 +417,18 @@ struct LegHot {
   bool done;
 };
 enum { kColdX, kColdU, kColdSu2, kColdSig, kColdDsu2, kColdRsu2, kColdT, kColdH, kColdN };
+// Threads per CTA of the persistent sampler.  Its results go to per-sample
+// slots (K1T reduces them in 256-sample tiles), so the CTA size is free: it is
+// chosen for the most resident warps at the kernel's register count.
+#ifndef ABLMC_AD_THREADS
+#define ABLMC_AD_THREADS 256
+#endif
+constexpr int kAdThreads = ABLMC_AD_THREADS;
 struct LegStore {
-  double d[kColdN][2][kTile];
-  long long steps[2][kTile];
-  int nrefl[2][kTile];
-  double pt[kPend][2][kTile], pe[kPend][2][kTile];  // GL/BAOAB only (SE launches without)
+  double d[kColdN][2][kAdThreads];
+  long long steps[2][kAdThreads];
+  int nrefl[2][kAdThreads];
+  double pt[kPend][2][kAdThreads], pe[kPend][2][kAdThreads];  // GL/BAOAB only (SE launches without)
 };
 template <int IG>
 constexpr size_t leg_store_bytes() {
@@ -591,7 +598,7 @@ __device__ __forceinline__ bool path_event(PathSM& S, const KernelArgs& a, uint6
 #define ABLMC_MINB_ADAPTIVE_SE ABLMC_MINB_ADAPTIVE
 #endif
 template <int IG, int PROF, bool COUPLED, int FAST>
-__global__ void __launch_bounds__(kTile, IG == kSE ? ABLMC_MINB_ADAPTIVE_SE : ABLMC_MINB_ADAPTIVE)
+__global__ void __launch_bounds__(kAdThreads, IG == kSE ? ABLMC_MINB_ADAPTIVE_SE : ABLMC_MINB_ADAPTIVE)
     k_adaptive_persistent(const KernelArgs a) {
   const DevModel& m = a.model;
   bool bad = false;
@@ -751,9 +758,10 @@ cudaError_t launch_adaptive(const KernelArgs& a, double* tile_sums, long long* t
   auto run = [&](auto kernel) {
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kTile, smem);
-    const unsigned grid = unsigned(std::min<int64_t>(tiles, int64_t(sms) * std::max(per_sm, 1)));
-    kernel<<<grid, kTile, smem, st>>>(a);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kAdThreads, smem);
+    const int64_t ctas = (a.n + kAdThreads - 1) / kAdThreads;
+    const unsigned grid = unsigned(std::min<int64_t>(ctas, int64_t(sms) * std::max(per_sm, 1)));
+    kernel<<<grid, kAdThreads, smem, st>>>(a);
   };
   if (fast && a.fast == kFastUnit) run(k_adaptive_persistent<IG, PROF, COUPLED, kFastUnit>);
   else if (fast) run(k_adaptive_persistent<IG, PROF, COUPLED, 1>);
