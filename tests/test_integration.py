@@ -54,3 +54,38 @@ def test_adapter_sharded_over_all_gpus_same_bits():
 
     assert len(levels(one.stdout)) == 4
     assert levels(many.stdout) == levels(one.stdout)
+
+
+@needs_demo
+@pytest.mark.gpu
+def test_adapter_drivers_match_reference_drivers():
+    """ablmc_b200::run_mlmc / run_stmc / decay_sweep (the reference's types in
+    and out, every level sampled on the device) next to the reference's own
+    drivers on its CPU sampler, same seed: the same levels, N_l, costs and
+    warnings; estimates and fits equal up to the rounding of the level sums
+    (estimators.hpp:230-432)."""
+    r = subprocess.run([str(DEMO), "drivers"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    rows = {}
+    for line in r.stdout.splitlines():
+        t = line.split()
+        if t[0] in ("mlmc", "stmc"):
+            rows[(t[0], t[1])] = t[2:]
+    for kind in ("mlmc", "stmc"):
+        g, c = rows[(kind, "gpu")], rows[(kind, "cpu")]
+        gi, ci = g.index("N_l"), c.index("N_l")
+        assert g[gi:] == c[ci:], (kind, g, c)  # N_l per level
+        named = lambda t: dict(zip(t[0:gi:2], t[1:gi:2]))
+        G, Cc = named(g), named(c)
+        for k in ("levels_used", "cost", "pilot", "failed", "warnings"):
+            assert G[k] == Cc[k], (kind, k, G[k], Cc[k])
+        for k in ("estimate", "stat_error", "bias", "alpha", "c1"):
+            a, b = float(G[k]), float(Cc[k])
+            assert abs(a - b) <= 1e-9 * abs(b) + 1e-15, (kind, k, a, b)
+    decay = [l.split() for l in r.stdout.splitlines() if l.startswith("decay") and "gpu" in l]
+    assert len(decay) == 3
+    for t in decay:
+        assert t[5:7] == t[10:12]  # n, cost_steps
+        for a, b in ((t[3], t[8]), (t[4], t[9])):
+            assert abs(float(a) - float(b)) <= 1e-9 * abs(float(b))
+    assert "decay empty 0" in r.stdout
