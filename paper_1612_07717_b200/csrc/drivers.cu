@@ -6,6 +6,7 @@
 // accumulate_samples call goes through ablmc_accumulate_samples /
 // ablmc_accumulate_paths (the device path); the drivers stay on the host,
 // as the north star asks.  Exceptions map to return codes (see ablmc_b200.h).
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -215,7 +216,7 @@ double now_s() {
 }
 
 void fill_levels(const std::vector<Stats>& levels, ablmc_run_result* out) {
-  out->n_levels = int(levels.size());
+  out->n_levels = int(std::min<size_t>(levels.size(), ABLMC_MAX_LEVELS));
   for (size_t l = 0; l < levels.size() && l < ABLMC_MAX_LEVELS; ++l) {
     out->level_n[l] = levels[l].n;
     out->level_failed[l] = levels[l].failed;
@@ -309,6 +310,15 @@ int ablmc_run_mlmc(const ablmc_problem* pr, double eps, const ablmc_mlmc_options
   ablmc_mlmc_options o;
   if (o_in) o = *o_in;
   else ablmc_mlmc_options_defaults(&o);
+  // ablmc_run_result holds ABLMC_MAX_LEVELS per-level rows (the reference's
+  // vector is unbounded; its default l_max is 16): refuse what cannot be
+  // reported instead of truncating
+  if (o.l_max < 0 || o.l_max >= ABLMC_MAX_LEVELS || o.pilot_levels_max < 0 ||
+      o.pilot_levels_max >= ABLMC_MAX_LEVELS) {
+    set_error("run_mlmc: l_max and pilot_levels_max must be in [0, " +
+              std::to_string(ABLMC_MAX_LEVELS - 1) + "]");
+    return ABLMC_ERR_INVALID_ARGUMENT;
+  }
   if (int rc = ablmc_check_se_stability(pr, pr->T / double(pr->m0))) return rc;
   const double t0 = now_s();
   clear_result(out);

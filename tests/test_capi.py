@@ -331,3 +331,16 @@ def test_adaptive_reference_height_validated(x_adapt):
     with pytest.raises(ValueError, match="x_adapt"):
         ablmc.Problem.make(ablmc.ModelParams(), ablmc.Integrator.gl, ablmc.QoISpec(), 0.3, 0.1,
                            1.0, 8, 3, opt)
+
+
+@pytest.mark.parametrize("field,value", [("l_max", capi.ABLMC_MAX_LEVELS), ("l_max", -1),
+                                         ("pilot_levels_max", capi.ABLMC_MAX_LEVELS)])
+def test_run_mlmc_refuses_levels_beyond_the_result_rows(field, value):
+    """ablmc_run_result has ABLMC_MAX_LEVELS per-level rows: options that could
+    produce more are an invalid argument (no truncation), checked before the
+    device is touched."""
+    pr = ablmc.Problem.make(ablmc.ModelParams(), ablmc.Integrator.gl, ablmc.QoISpec(), 0.5, 0.1,
+                            1.0, 1, 1)
+    o = ablmc.MlmcOptions(**{field: value})
+    with pytest.raises(ValueError, match="l_max and pilot_levels_max"):
+        ablmc.run_mlmc(pr, 1e-3, o)
