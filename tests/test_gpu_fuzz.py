@@ -132,3 +132,30 @@ def test_deep_pending_pairs_bit_exact():
             O.orc().orc_set_device_math(0)
         assert deep > 0, ig  # the problem does exercise K1D
 
+
+
+def test_random_problems_vs_the_unmodified_reference():
+    """tools/fuzz_reference.py on 400 fixed trials (the first slice of the
+    campaign recorded in profiles/r2_fuzz_reference.txt): random uniform-grid
+    problems on the reference profile, the device against oracle/_ref (the
+    reference headers themselves).  Oracle mode (host-supplied normals): every
+    failure flag, parity and reflection count equal, SE bit-identical, GL/BAOAB
+    within the north-star 1e-12; Philox mode within 1e-10."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    if O.ref() is None:
+        pytest.skip("oracle/_ref not built (needs /root/reference at build time)")
+    r = subprocess.run([sys.executable, str(root / "tools" / "fuzz_reference.py"), "0", "400"],
+                       capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stdout + r.stderr
+    lines = {l.split(":")[0]: l for l in r.stdout.splitlines() if ":" in l}
+    assert " 0 outside tolerance" in lines["oracle"], lines["oracle"]
+    assert " 0 parity / reflection-count mismatches" in lines["oracle"], lines["oracle"]
+    assert " 0 outside tolerance" in lines["philox"], lines["philox"]
+    assert " 0 flag mismatches" in lines["fuzz_reference"], lines["fuzz_reference"]
+    # SE in oracle mode: every pair bit-identical
+    se = lines["oracle"].split("se [")[1].split("]")[0].split(",")
+    assert int(se[0]) > 1000 and se[0].strip() == se[1].strip() and int(se[2]) == 0, lines["oracle"]
