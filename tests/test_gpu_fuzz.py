@@ -159,3 +159,22 @@ def test_random_problems_vs_the_unmodified_reference():
     # SE in oracle mode: every pair bit-identical
     se = lines["oracle"].split("se [")[1].split("]")[0].split(",")
     assert int(se[0]) > 1000 and se[0].strip() == se[1].strip() and int(se[2]) == 0, lines["oracle"]
+
+
+@pytest.mark.parametrize("tool,trials", [("fuzz_paths.py", 200), ("fuzz_binned.py", 120),
+                                         ("fuzz_campaign.py", 150)])
+def test_campaign_tools_first_slice(tool, trials):
+    """The first slice of the long campaigns recorded under profiles/
+    (tools/fuzz_paths.py: single-path samplers incl. the lean level-0 and
+    short-path kernels; tools/fuzz_binned.py: the binned-field QoI / K4;
+    tools/fuzz_campaign.py: coupled pairs with wider ranges): device vs the C
+    oracle on the device's elementary functions, no mismatch."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    r = subprocess.run([sys.executable, str(root / "tools" / tool), "0", str(trials)],
+                       capture_output=True, text=True, timeout=900, cwd=root)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert ", 0 mismatches" in r.stdout
