@@ -10,7 +10,13 @@ fresh seeds), two legs per problem:
 Parities, reflection counts and failure flags must agree.  Pairs outside the
 tolerance are listed, not hidden (a 1-ulp libm difference can tip a
 reflection for a path that lands within an ulp of a wall).
-usage: python tools/fuzz_reference.py [first_trial] [n_trials]"""
+With --adaptive: adaptive (non-nested) problems only, Philox mode only (the
+adaptive draws are data dependent, so there is no host-normal mode): the
+schedule's comparisons see normals that differ from glibc's by an ulp, so a
+pair's step sequence can legitimately differ; the share of pairs within
+1e-10 is reported, and the run never fails on it (tests/test_gpu_adaptive.py
+bounds the share by the reference's own 1-ulp sensitivity).
+usage: python tools/fuzz_reference.py [first_trial] [n_trials] [--adaptive]"""
 import ctypes as C
 import sys
 import time
@@ -23,8 +29,10 @@ import oracle_lib as O  # noqa: E402
 from paper_1612_07717_b200 import ablmc, capi  # noqa: E402
 from test_gpu_fuzz import Ig, random_problem  # noqa: E402
 
-first_trial = int(sys.argv[1]) if len(sys.argv) > 1 else 0
-n_trials = int(sys.argv[2]) if len(sys.argv) > 2 else 500
+ADAPTIVE = "--adaptive" in sys.argv
+argv = [a for a in sys.argv[1:] if not a.startswith("--")]
+first_trial = int(argv[0]) if len(argv) > 0 else 0
+n_trials = int(argv[1]) if len(argv) > 1 else 500
 R = O.ref()
 assert R is not None, "oracle/_ref/libablmc_ref.so missing (built where /root/reference exists)"
 ablmc.init(0)
@@ -47,18 +55,22 @@ for trial in range(first_trial, first_trial + n_trials):
     except Exception:
         continue
     c = pr._c
-    if c.adaptive or c.profile != 0:
+    if bool(c.adaptive) != ADAPTIVE or c.profile != 0:
         continue
     if rng.random() < 0.3:
         level = int(rng.integers(1, 6))
     M = c.m0 << level
+    if ADAPTIVE and M > 640:
+        continue
     first = int(rng.integers(0, 2**40))
     problems += 1
     want = (capi.PairStateC * n)()
     R.ref_pair_states(C.byref(c), level, first, n, want)
-    xi = np.stack([O.ref_normals(c.seed, level, first + i, 0, M) for i in range(n)])
-    for mode, got in (("oracle", ablmc.simulate_pairs(pr, level, first, n, xi=xi)),
-                      ("philox", ablmc.simulate_pairs(pr, level, first, n))):
+    legs = [("philox", ablmc.simulate_pairs(pr, level, first, n))]
+    if not ADAPTIVE:
+        xi = np.stack([O.ref_normals(c.seed, level, first + i, 0, M) for i in range(n)])
+        legs.insert(0, ("oracle", ablmc.simulate_pairs(pr, level, first, n, xi=xi)))
+    for mode, got in legs:
         tol = 1e-12 if mode == "oracle" else 1e-10
         S = stats[mode]
         for i in range(n):
@@ -100,4 +112,4 @@ for m, S in stats.items():
 print(f"fuzz_reference: trials {first_trial}..{first_trial + n_trials - 1}: {problems} problems vs "
       f"the unmodified reference, {failed_paths} failed paths agreed, {len(flags_bad)} flag "
       f"mismatches, {time.time() - t0:.0f} s")
-sys.exit(1 if flags_bad or stats["oracle"]["out"] else 0)
+sys.exit(1 if (flags_bad or stats["oracle"]["out"]) and not ADAPTIVE else 0)
