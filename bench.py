@@ -471,6 +471,10 @@ def run_b200(a):
         raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dist_on = world > 1 or a.force_dist
+    if dist_on and "RANK" not in os.environ:
+        # --force-dist outside torchrun: a one-rank group on the loopback
+        os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
+                          MASTER_PORT=str(free_port()))
     if dist_on:
         # torch.distributed is the plumbing here (barriers, max over ranks,
         # shipping the NCCL unique id); the data path is the library's own NCCL

@@ -84,6 +84,12 @@ def init_devices(n: int, devices: Sequence[int] | None = None) -> None:
     _check(lib().ablmc_init_devices(int(n), devs))
 
 
+def init_loopback(n: int, device: int = 0) -> None:
+    """Verification transport: n ranks sharing ONE device, the all-gather as
+    device-to-device copies (include/ablmc_b200.h, ablmc_init_loopback)."""
+    _check(lib().ablmc_init_loopback(int(n), int(device)))
+
+
 def nccl_unique_id() -> bytes:
     """ncclUniqueId for ablmc_init_group (rank 0 creates it and ships it)."""
     buf = (C.c_ubyte * capi.ABLMC_NCCL_ID_BYTES)()

@@ -118,6 +118,7 @@ SIGNATURES = {
     "ablmc_nccl_unique_id": (C.c_int, [P(C.c_ubyte)]),
     "ablmc_init_group": (C.c_int, [C.c_int, C.c_int, C.c_int, P(C.c_ubyte)]),
     "ablmc_init_devices": (C.c_int, [C.c_int, P(C.c_int)]),
+    "ablmc_init_loopback": (C.c_int, [C.c_int, C.c_int]),
     "ablmc_group_info": (C.c_int, [P(C.c_int), P(C.c_int), P(C.c_int), P(C.c_int)]),
     "ablmc_last_collective_count": (C.c_int64, []),
     "ablmc_gather_layout": (C.c_int, [C.c_int, C.c_int, C.c_int, P(C.c_int64), P(C.c_int64),

@@ -4,7 +4,11 @@ all-gather per accumulate call / per accumulate_levels batch): bit-identical
 to the single-device calls.  On a one-GPU box the clique has one member, so
 this exercises the packing, the NCCL all-gather, the status row and both
 merges (host and device-resident) at world size 1; tests/test_sharding.py
-covers the layout and merge for world sizes 2-3 on CPU."""
+covers the layout and merge for world sizes 2-3 on CPU, and the loopback
+transport below (ablmc_init_loopback: n ranks sharing the one device, the
+all-gather as device-to-device copies) runs the same workload at world sizes
+2, 3 and 8 -- per-rank ranges, packed rows, status rows, both merges -- on the
+device, everything but the NCCL call itself."""
 import ctypes as C
 
 import numpy as np
@@ -74,6 +78,30 @@ def test_init_devices_native_nccl_is_bit_identical():
         if not k.endswith("collectives"):
             assert grouped[k] == single[k], k
     assert ablmc.group_info()["mode"] == 0
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_loopback_world_sizes_bit_identical(world):
+    """World sizes > 1 on one GPU: the ranks' shares (some empty: requests of
+    fewer super-blocks than ranks), the packed blocks, the device-resident
+    grouped merge and the host merge give the single-device bits."""
+    pr = ablmc.Problem.make(ablmc.ModelParams(), ablmc.Integrator.gl, ablmc.QoISpec(), 0.05, 0.1,
+                            1.0, 2, 21)
+    q = ablmc.QoISpec(kind=ablmc.QoIKind.binned_field, bin_edges=ablmc.equidistant_edges(16, 1.0))
+    prb = ablmc.Problem.make(ablmc.ModelParams(), ablmc.Integrator.baoab, q, 0.05, 0.1, 1.0, 4, 9)
+    count = 5 * (1 << 22) + 777
+    ablmc.init(0)
+    single = _workload(pr, prb, count)
+    try:
+        ablmc.init_loopback(world, 0)
+        assert ablmc.group_info() == {"mode": 3, "rank": 0, "world": world, "n_local": world}
+        grouped = _workload(pr, prb, count)
+    finally:
+        ablmc.init(0)
+    assert grouped["samples_collectives"] == 1 and grouped["levels_collectives"] == 1
+    for k in single:
+        if not k.endswith("collectives"):
+            assert grouped[k] == single[k], k
 
 
 def test_init_group_world_one_and_errors():
