@@ -368,6 +368,7 @@ def configs_sweep(lib, stream):
     extension profiles).  Each level is one device accumulate call of N
     samples (config 4 bounded to 2^22 paths per level instead of 2e8, to keep
     the default run short; throughput is per path, so it extrapolates)."""
+    import torch
     from paper_1612_07717_b200 import ablmc
     out = {}
     mp = ablmc.ModelParams()
@@ -390,7 +391,19 @@ def configs_sweep(lib, stream):
             ms, n, cost = _timed_level(lib, stream, pr, level, 1000000)
             total_ms += ms
             rows.append({"level": level, "ms": ms, "cost_steps": cost})
+        # the same nine levels as ONE accumulate_levels batch through the public
+        # API (what one MLMC allocation round is: the levels run on concurrent
+        # lanes, one synchronisation, host LevelStats out): wall time, best of 3
+        walls = []
+        for _ in range(4):
+            reqs = [(ablmc.LevelStats().init(l, pr.h_level(l), 1), 0, 1000000, l) for l in range(9)]
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ablmc.accumulate_levels(reqs, pr)
+            walls.append((time.perf_counter() - t0) * 1e3)
+        assert [r[0].cost_steps for r in reqs] == [r["cost_steps"] for r in rows]
         c2[ig.name] = {"levels": rows, "total_ms": total_ms,
+                       "one_batch_wall_ms": min(walls[1:]),
                        "fine_path_steps_per_s_level8": 1e6 * 256 / (rows[-1]["ms"] * 1e-3)}
     out["config2_floored_levels0to8_1e6"] = c2
     # config 4: release at z0 = 10 m, 64-bin smoothed concentration field,
