@@ -124,3 +124,44 @@ def test_init_group_world_one_and_errors():
         ablmc.init(0)
     assert _key(grp) == _key(one)
     assert np.isfinite(one.mean())
+
+
+def test_calls_from_several_host_threads_are_serialised():
+    """Concurrent accumulate calls from four host threads (ctypes drops the
+    GIL): the library's lock serialises them; every result equals the
+    single-threaded one bit for bit."""
+    import threading
+
+    ablmc.init(0)
+    prs = [ablmc.Problem.make(ablmc.ModelParams(), ig, ablmc.QoISpec(), 0.3 + 0.1 * i, 0.1, 1.0, 2,
+                              100 + i)
+           for i, ig in enumerate((ablmc.Integrator.se, ablmc.Integrator.gl, ablmc.Integrator.baoab,
+                                   ablmc.Integrator.se))]
+    jobs = [(i, level, 50000 + 1000 * level + i) for i in range(4) for level in (0, 1, 3, 5)]
+
+    def run(i, level, count):
+        a = ablmc.LevelStats().init(level, prs[i].h_level(level), 1)
+        ablmc.accumulate_samples(a, 3 * i, count, prs[i], level)
+        return _key(a)
+
+    serial = {j: run(*j) for j in jobs}
+    got, errs = {}, []
+
+    def worker(i):
+        try:
+            for _ in range(5):
+                for j in jobs:
+                    if j[0] == i:
+                        got[(j, _)] = run(*j)
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    ts = [threading.Thread(target=worker, args=(i,)) for i in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    assert len(got) == 5 * len(jobs)
+    for (j, _), k in got.items():
+        assert k == serial[j], j
